@@ -1,0 +1,150 @@
+/*
+ * vmt19937_b200.h -- C ABI of the B200-native VMT19937 generator.
+ *
+ * Drop-in boundary for the reference's generation path.
+ * The reference exposes a C++ surface only (no C ABI, no FFI); each entry point
+ * below names the reference interface it replaces. All functions return a
+ * vmt_status (0 = success) and never throw; the three reference exception
+ * classes map to VMT_EINVAL (std::invalid_argument), VMT_ESTATE
+ * (std::logic_error) and VMT_EIO (std::runtime_error), plus VMT_ECUDA.
+ *
+ * Threading: one owner per handle, like VmtEngine; distinct
+ * handles are independent. Buffers are caller-owned; every fill takes an
+ * explicit length (the reference's sizes are implicit, engine.hpp:77,92).
+ * Destination pointers may be device memory or host memory (pinned or
+ * pageable); host destinations are filled through device staging.
+ * Streams are cudaStream_t passed as void* (NULL = the handle's own stream).
+ */
+#ifndef VMT19937_B200_H
+#define VMT19937_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct vmt_generator* vmt_handle;
+
+enum vmt_status {
+    VMT_OK = 0,
+    VMT_EINVAL = -1, /* std::invalid_argument (engine.hpp:29-32, jump.cpp:9-10) */
+    VMT_ESTATE = -2, /* std::logic_error (engine.hpp:93-94, jump.cpp:30-31)     */
+    VMT_EIO = -3,    /* std::runtime_error (jump_file.cpp:76-88)                */
+    VMT_ECUDA = -4,  /* CUDA runtime failure (no device, launch error, OOM)     */
+    VMT_ENOMEM = -5
+};
+
+/* QueryMode (engine.hpp:15) -- accepted for API parity; every mode emits the
+ * same stream (test_engine.cpp:81-109). */
+enum vmt_query_mode { VMT_QUERY_SINGLE = 0, VMT_QUERY_BLOCK16 = 1, VMT_QUERY_STATE_BLOCK = 2 };
+
+/* Floating-point conversion rules (the reference has none: SURVEY.md G2/A16).
+ * All are exact in IEEE arithmetic, so GPU and CPU agree bit for bit. */
+enum vmt_real_rule {
+    VMT_F32_24 = 0,    /* float  (x >> 8) * 2^-24            in [0,1)                      */
+    VMT_F64_32 = 1,    /* double x * 2^-32                   in [0,1)  (genrand_real2)      */
+    VMT_F64_REAL3 = 2, /* double (x + 0.5) * 2^-32           in (0,1)  (stats.cpp:118)      */
+    VMT_F64_RES53 = 3  /* double ((a>>5)*2^26+(b>>6))*2^-53  in [0,1), 2 words per value    */
+};
+
+/* Pass as jump_exponent to get the library default (JumpSpec::full_period_exponent). */
+#define VMT_FULL_PERIOD 0xFFFFFFFFu
+
+/* JumpSpec::full_period_exponent (jump.cpp:13-15): 19937 - log2(lanes). */
+unsigned vmt_full_period_exponent(unsigned lanes);
+
+/* VmtEngine<M>(seed, F^(2^q), q) (engine.hpp:54-63) / VmtGenerator
+ * (engine.hpp:162-167): seeds MT19937 (mt19937.cpp:22-27) and de-phases lane
+ * t by t*2^q steps (make_dephased_states, jump.cpp:35-53) with a polynomial
+ * jump on the GPU. lanes in {1,2,4,8,16,32} (32 lifts engine.hpp:43, G1).
+ * jump_exponent: any q, or VMT_FULL_PERIOD. device: CUDA ordinal. */
+int vmt_create(uint32_t seed, unsigned lanes, unsigned jump_exponent, int device, vmt_handle* out);
+
+/* Adopts caller-supplied boundary lane states (lanes x 624 words, lane-major,
+ * Mt19937::from_words semantics, mt19937.cpp:29-34) as the generator's start. */
+int vmt_create_from_states(const uint32_t* lane_states, unsigned lanes, int device, vmt_handle* out);
+
+int vmt_destroy(vmt_handle h);
+
+unsigned vmt_lanes(vmt_handle h);              /* VmtEngine::lanes (engine.hpp:47)          */
+uint64_t vmt_state_words(vmt_handle h);        /* VmtEngine::state_words (engine.hpp:48)    */
+unsigned vmt_jump_exponent(vmt_handle h);      /* VmtEngine::jump_exponent (engine.hpp:100) */
+uint64_t vmt_position(vmt_handle h);           /* words consumed so far                     */
+
+/* VmtEngine::next_u32 (engine.hpp:70-74). */
+int vmt_next_u32(vmt_handle h, uint32_t* out);
+/* VmtEngine::next_block16 (engine.hpp:77-87): exactly 16 words. */
+int vmt_next_block16(vmt_handle h, uint32_t* out16);
+/* VmtEngine::next_block_state (engine.hpp:92-98): exactly 624*lanes words;
+ * VMT_ESTATE off a state-block boundary (engine.hpp:93-94). */
+int vmt_next_block_state(vmt_handle h, uint32_t* out);
+
+/* Next n stream words (any n; next_u32 continuation semantics). */
+int vmt_fill_u32(vmt_handle h, uint32_t* dst, uint64_t n, void* stream);
+/* Next n values converted by rule (VMT_F32_24). */
+int vmt_fill_f32(vmt_handle h, float* dst, uint64_t n, int rule, void* stream);
+/* Next n values converted by rule (VMT_F64_32 / VMT_F64_REAL3 / VMT_F64_RES53;
+ * RES53 consumes 2n words and needs an even stream position). */
+int vmt_fill_f64(vmt_handle h, double* dst, uint64_t n, int rule, void* stream);
+/* XOR fold of the next n words without storing them (bench.cpp:13-18 fold;
+ * fused no-store consumer). */
+int vmt_checksum_xor(vmt_handle h, uint64_t n, uint32_t* out, void* stream);
+
+/* Waits for all work this handle enqueued (device fills are asynchronous). */
+int vmt_synchronize(vmt_handle h);
+
+/* Advances the position by d words (new; arbitrary 64-bit distance). */
+int vmt_skip(vmt_handle h, uint64_t d);
+
+/* VmtEngine::interleaved_state (engine.hpp:100): 624*lanes words, state of
+ * the most recently regenerated block (the de-phased seed states before the
+ * first query). */
+int vmt_export_state(vmt_handle h, uint32_t* out);
+
+/* Batch of ngen independent generators with seeds seed0..seed0+ngen-1 (config
+ * 3): dst[g*n_per_gen + i] = word i of generator g (generator-major). */
+int vmt_batch_fill_u32(uint32_t seed0, unsigned ngen, unsigned lanes, unsigned jump_exponent,
+                       uint64_t n_per_gen, uint32_t* dst, int device, void* stream);
+
+/* jump_state (jump.cpp:27-33) generalised to arbitrary 64-bit distances, for
+ * n boundary states (n x 624 words, lane-major; host or device memory):
+ * dst_i = src_i advanced by distances[i] steps (config 5). */
+int vmt_jump_states(const uint32_t* src, uint64_t n, const uint64_t* distances, uint32_t* dst,
+                    int device, void* stream);
+
+/* Seeds n MT19937 states (init_genrand) into dst (n x 624, lane-major). */
+int vmt_seed_states(const uint32_t* seeds, uint64_t n, uint32_t* dst, int device, void* stream);
+
+/* Jump polynomials (host): x^d mod P and x^(2^q) mod P as 312 little-endian
+ * u64 words; the characteristic polynomial P as 313 words. */
+int vmt_jump_poly(uint64_t d_lo, uint64_t d_hi, uint64_t* out312);
+int vmt_jump_poly_pow2(unsigned q, uint64_t* out312);
+int vmt_charpoly(uint64_t* out313);
+
+/* Kernel tuning for the generation path: chunks per fill (0 = auto), and
+ * the CTA shape variant (0 = auto). Returns VMT_EINVAL for unknown variants. */
+int vmt_set_tuning(vmt_handle h, unsigned max_chunks, int variant);
+
+/* Profiling: when enabled, each fill records CUDA events on its stream around
+ * the chunk-positioning jumps and the generation kernel; vmt_last_timings
+ * returns both durations (ms) of the most recent fill. */
+int vmt_set_profiling(vmt_handle h, int enable);
+int vmt_last_timings(vmt_handle h, float* jump_ms, float* gen_ms);
+
+/* Counters: kernels launched by this handle so far (generation, jump, seed,
+ * reduce), and the number of lane-state jumps performed. */
+int vmt_stats(vmt_handle h, uint64_t* gen_launches, uint64_t* jump_launches, uint64_t* other_launches,
+              uint64_t* lane_jumps);
+
+const char* vmt_status_string(int status);
+/* Message of the last failure on this thread. */
+const char* vmt_last_error(void);
+int vmt_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VMT19937_B200_H */

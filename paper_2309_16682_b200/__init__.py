@@ -1,0 +1,314 @@
+"""B200-native VMT19937 (arXiv 2309.16682): host-side mirror of the reference
+generator interface over the C ABI (include/vmt19937_b200.h).
+
+Reference names are kept (proj/include/vmt19937/engine.hpp, jump.hpp):
+
+* ``JumpSpec``      jump.hpp:13-21 (full_period_exponent: jump.cpp:13-15)
+* ``QueryMode``     engine.hpp:15
+* ``VmtConfig``     engine.hpp:18-33 (lanes 1..32; 32 lifts engine.hpp:29-32, G1)
+* ``VmtGenerator``  engine.hpp:160-207; ``VmtEngine(lanes, seed, q)`` is the
+  fixed-lane spelling of engine.hpp:41-68
+* ``next_u32 / next_block16 / next_block_state / interleaved_state`` engine.hpp:70-101
+* new: ``fill_u32 / fill_f32 / fill_f64 / checksum_xor / skip`` (bulk GPU
+  output, any length), ``batch_fill_u32`` (config 3), ``jump_states`` (config 5)
+
+Buffers may be torch tensors (CUDA or CPU) or numpy arrays. Every word is
+produced by the sm_100a kernels; there is no CPU generation path.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+from typing import Optional
+
+import numpy as np
+
+from . import _capi
+from ._capi import (VMT_F32_24, VMT_F64_32, VMT_F64_RES53, VMT_F64_REAL3, VMT_FULL_PERIOD,
+                    InvalidArgument, LogicError, VmtError, check, lib)
+
+__all__ = [
+    "JumpSpec", "QueryMode", "VmtConfig", "VmtGenerator", "VmtEngine", "batch_fill_u32",
+    "jump_states", "seed_states", "charpoly", "jump_poly", "jump_poly_pow2", "VmtError",
+    "InvalidArgument", "LogicError", "VMT_F32_24", "VMT_F64_32", "VMT_F64_REAL3", "VMT_F64_RES53",
+    "KEFFECTIVE_BITS", "KSTATE_LEN",
+]
+
+KSTATE_LEN = 624
+KEFFECTIVE_BITS = 19937
+
+
+class QueryMode(enum.IntEnum):
+    kSingle = 0
+    kBlock16 = 1
+    kStateBlock = 2
+
+
+class JumpSpec:
+    """Stream splitting: lane t de-phased by t * 2^exponent (jump.hpp:13-21)."""
+
+    def __init__(self, exponent: int, lanes: int):
+        self.exponent = exponent
+        self.lanes = lanes
+
+    def validate(self) -> None:
+        if self.lanes < 1 or (self.lanes & (self.lanes - 1)):
+            raise InvalidArgument(_capi.VMT_EINVAL, "lanes must be a power of two")
+
+    @staticmethod
+    def full_period_exponent(lanes: int) -> int:
+        return int(lib.vmt_full_period_exponent(lanes))
+
+    def is_full_period_split(self) -> bool:
+        return self.exponent == self.full_period_exponent(self.lanes)
+
+    @classmethod
+    def full_period_split(cls, lanes: int) -> "JumpSpec":
+        s = cls(cls.full_period_exponent(lanes), lanes)
+        s.validate()
+        return s
+
+
+class VmtConfig:
+    """engine.hpp:18-33; jump_exponent defaults to the full-period split."""
+
+    def __init__(self, lanes: int, mode: QueryMode = QueryMode.kSingle, jump_exponent: Optional[int] = None):
+        self.lanes = lanes
+        self.mode = mode
+        self.jump_exponent = JumpSpec.full_period_exponent(lanes) if jump_exponent is None else jump_exponent
+
+    def validate(self) -> None:
+        if self.lanes not in (1, 2, 4, 8, 16, 32):
+            raise InvalidArgument(_capi.VMT_EINVAL, "lanes must be one of 1, 2, 4, 8, 16, 32")
+
+
+def _ptr(buf) -> tuple[int, object, int, str]:
+    """(address, keepalive, element count, kind) of a torch tensor / numpy array."""
+    try:
+        import torch  # noqa: F401
+        if isinstance(buf, torch.Tensor):
+            if not buf.is_contiguous():
+                raise InvalidArgument(_capi.VMT_EINVAL, "buffer must be contiguous")
+            return buf.data_ptr(), buf, buf.numel(), ("cuda" if buf.is_cuda else "cpu")
+    except ImportError:
+        pass
+    if isinstance(buf, np.ndarray):
+        if not buf.flags["C_CONTIGUOUS"]:
+            raise InvalidArgument(_capi.VMT_EINVAL, "buffer must be contiguous")
+        return buf.ctypes.data, buf, buf.size, "cpu"
+    raise InvalidArgument(_capi.VMT_EINVAL, f"unsupported buffer type {type(buf)!r}")
+
+
+def _stream_for(kind: str, stream) -> Optional[int]:
+    if stream is not None:
+        return int(stream)
+    if kind == "cuda":
+        import torch
+        s = torch.cuda.current_stream().cuda_stream
+        # torch's default stream is the legacy NULL stream; NULL in the C ABI
+        # means "the handle's own stream", so name the legacy stream explicitly
+        return s if s else CUDA_STREAM_LEGACY
+    return None
+
+
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
+
+
+def _check_dtype(buf, np_dtype, torch_name: str) -> None:
+    dt = getattr(buf, "dtype", None)
+    if isinstance(buf, np.ndarray):
+        if buf.dtype != np_dtype:
+            raise InvalidArgument(_capi.VMT_EINVAL, f"expected {np.dtype(np_dtype)} buffer")
+    else:
+        if str(dt) != f"torch.{torch_name}":
+            raise InvalidArgument(_capi.VMT_EINVAL, f"expected torch.{torch_name} buffer, got {dt}")
+
+
+class VmtGenerator:
+    """Runtime-lane-count VMT19937 generator on one GPU (engine.hpp:160-207)."""
+
+    def __init__(self, seed: int, cfg: Optional[VmtConfig] = None, device: int = 0, *, lane_states=None):
+        self._h = ctypes.c_void_p()
+        if lane_states is not None:
+            arr = np.ascontiguousarray(lane_states, dtype=np.uint32)
+            lanes = arr.size // KSTATE_LEN
+            check(lib.vmt_create_from_states(arr.ctypes.data, lanes, device, ctypes.byref(self._h)))
+            self.cfg = VmtConfig(lanes, QueryMode.kSingle, 0)
+        else:
+            cfg = cfg or VmtConfig(1)
+            cfg.validate()
+            self.cfg = cfg
+            check(lib.vmt_create(seed & 0xFFFFFFFF, cfg.lanes, cfg.jump_exponent, device, ctypes.byref(self._h)))
+        self.device = device
+
+    # -- lifetime -------------------------------------------------------------
+    def close(self) -> None:
+        if self._h:
+            check(lib.vmt_destroy(self._h))
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- reference properties -------------------------------------------------
+    @property
+    def lanes(self) -> int:
+        return int(lib.vmt_lanes(self._h))
+
+    @property
+    def state_words(self) -> int:
+        return int(lib.vmt_state_words(self._h))
+
+    buffer_words = 16
+
+    def jump_exponent(self) -> int:
+        return int(lib.vmt_jump_exponent(self._h))
+
+    @property
+    def position(self) -> int:
+        return int(lib.vmt_position(self._h))
+
+    # -- reference queries (engine.hpp:70-98) ---------------------------------
+    def next_u32(self) -> int:
+        v = ctypes.c_uint32()
+        check(lib.vmt_next_u32(self._h, ctypes.byref(v)))
+        return v.value
+
+    def next_block16(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        out = np.empty(16, np.uint32) if out is None else out
+        check(lib.vmt_next_block16(self._h, out.ctypes.data))
+        return out
+
+    def next_block_state(self, out=None):
+        out = np.empty(self.state_words, np.uint32) if out is None else out
+        addr, _, n, _ = _ptr(out)
+        if n < self.state_words:
+            raise InvalidArgument(_capi.VMT_EINVAL, "buffer smaller than state_words")
+        check(lib.vmt_next_block_state(self._h, addr))
+        return out
+
+    def interleaved_state(self) -> np.ndarray:
+        out = np.empty(self.state_words, np.uint32)
+        check(lib.vmt_export_state(self._h, out.ctypes.data))
+        return out
+
+    # -- bulk GPU output ------------------------------------------------------
+    def fill_u32(self, out, n: Optional[int] = None, stream=None):
+        addr, keep, size, kind = _ptr(out)
+        _check_dtype(out, np.uint32, "uint32")
+        n = size if n is None else n
+        if n > size:
+            raise InvalidArgument(_capi.VMT_EINVAL, "n exceeds buffer size")
+        check(lib.vmt_fill_u32(self._h, addr, n, _stream_for(kind, stream)))
+        return out
+
+    def fill_f32(self, out, n: Optional[int] = None, rule: int = VMT_F32_24, stream=None):
+        addr, keep, size, kind = _ptr(out)
+        _check_dtype(out, np.float32, "float32")
+        n = size if n is None else n
+        check(lib.vmt_fill_f32(self._h, addr, n, rule, _stream_for(kind, stream)))
+        return out
+
+    def fill_f64(self, out, n: Optional[int] = None, rule: int = VMT_F64_32, stream=None):
+        addr, keep, size, kind = _ptr(out)
+        _check_dtype(out, np.float64, "float64")
+        n = size if n is None else n
+        check(lib.vmt_fill_f64(self._h, addr, n, rule, _stream_for(kind, stream)))
+        return out
+
+    def checksum_xor(self, n: int, stream=None) -> int:
+        v = ctypes.c_uint32()
+        check(lib.vmt_checksum_xor(self._h, n, ctypes.byref(v), None if stream is None else int(stream)))
+        return v.value
+
+    def synchronize(self) -> None:
+        check(lib.vmt_synchronize(self._h))
+
+    def skip(self, d: int) -> None:
+        check(lib.vmt_skip(self._h, d))
+
+    def set_tuning(self, max_chunks: int = 0, variant: int = 0) -> None:
+        check(lib.vmt_set_tuning(self._h, max_chunks, variant))
+
+    def set_profiling(self, enable: bool = True) -> None:
+        check(lib.vmt_set_profiling(self._h, int(enable)))
+
+    def last_timings(self) -> tuple[float, float]:
+        """(jump_ms, gen_ms) of the most recent fill (profiling enabled)."""
+        a, b = ctypes.c_float(), ctypes.c_float()
+        check(lib.vmt_last_timings(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def stats(self) -> dict:
+        vals = [ctypes.c_uint64() for _ in range(4)]
+        check(lib.vmt_stats(self._h, *[ctypes.byref(v) for v in vals]))
+        return dict(zip(("gen_launches", "jump_launches", "other_launches", "lane_jumps"),
+                        (v.value for v in vals)))
+
+
+def VmtEngine(lanes: int, seed: int, jump_exponent: Optional[int] = None, device: int = 0) -> VmtGenerator:
+    """VmtEngine<M>(seed, F^(2^q), q) (engine.hpp:54); M=1 needs no jump."""
+    return VmtGenerator(seed, VmtConfig(lanes, QueryMode.kSingle, jump_exponent if lanes > 1 else 0), device)
+
+
+def batch_fill_u32(out, seed0: int, ngen: int, lanes: int, n_per_gen: int,
+                   jump_exponent: Optional[int] = None, device: int = 0, stream=None):
+    """ngen generators seeded seed0.. (config 3): out[g*n_per_gen + i]."""
+    addr, keep, size, kind = _ptr(out)
+    _check_dtype(out, np.uint32, "uint32")
+    if size < ngen * n_per_gen:
+        raise InvalidArgument(_capi.VMT_EINVAL, "buffer too small")
+    q = VMT_FULL_PERIOD if jump_exponent is None else jump_exponent
+    check(lib.vmt_batch_fill_u32(seed0, ngen, lanes, q, n_per_gen, addr, device, _stream_for(kind, stream)))
+    return out
+
+
+def jump_states(states, distances, out=None, device: int = 0, stream=None):
+    """Advance n boundary states (n x 624, lane-major) by 64-bit distances (config 5)."""
+    st = states
+    if isinstance(states, np.ndarray):
+        st = np.ascontiguousarray(states, np.uint32)
+    saddr, _, ssize, kind = _ptr(st)
+    n = ssize // KSTATE_LEN
+    d = np.ascontiguousarray(distances, np.uint64)
+    if d.size != n:
+        raise InvalidArgument(_capi.VMT_EINVAL, "one distance per state")
+    if out is None:
+        out = np.empty((n, KSTATE_LEN), np.uint32) if kind == "cpu" else st.new_empty(st.shape)
+    oaddr, _, _, _ = _ptr(out)
+    check(lib.vmt_jump_states(saddr, n, d.ctypes.data, oaddr, device, _stream_for(kind, stream)))
+    return out
+
+
+def seed_states(seeds, device: int = 0) -> np.ndarray:
+    s = np.ascontiguousarray(seeds, np.uint32)
+    out = np.empty((s.size, KSTATE_LEN), np.uint32)
+    check(lib.vmt_seed_states(s.ctypes.data, s.size, out.ctypes.data, device, None))
+    return out
+
+
+def charpoly() -> np.ndarray:
+    out = np.empty(313, np.uint64)
+    check(lib.vmt_charpoly(out.ctypes.data))
+    return out
+
+
+def jump_poly(d: int) -> np.ndarray:
+    out = np.empty(312, np.uint64)
+    check(lib.vmt_jump_poly(d & 0xFFFFFFFFFFFFFFFF, d >> 64, out.ctypes.data))
+    return out
+
+
+def jump_poly_pow2(q: int) -> np.ndarray:
+    out = np.empty(312, np.uint64)
+    check(lib.vmt_jump_poly_pow2(q, out.ctypes.data))
+    return out

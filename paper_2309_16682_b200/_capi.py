@@ -1,0 +1,105 @@
+"""ctypes binding of the C ABI in include/vmt19937_b200.h.
+
+Loads the in-tree libvmt19937_b200.so. There is deliberately no fallback: if
+the library is missing the import fails, and without a CUDA device every
+generating call raises VmtError(VMT_ECUDA).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libvmt19937_b200.so")
+
+VMT_OK, VMT_EINVAL, VMT_ESTATE, VMT_EIO, VMT_ECUDA, VMT_ENOMEM = 0, -1, -2, -3, -4, -5
+VMT_FULL_PERIOD = 0xFFFFFFFF
+VMT_F32_24, VMT_F64_32, VMT_F64_REAL3, VMT_F64_RES53 = 0, 1, 2, 3
+
+# every symbol include/vmt19937_b200.h declares
+EXPORTS = [
+    "vmt_full_period_exponent", "vmt_create", "vmt_create_from_states", "vmt_destroy", "vmt_lanes",
+    "vmt_state_words", "vmt_jump_exponent", "vmt_position", "vmt_next_u32", "vmt_next_block16",
+    "vmt_next_block_state", "vmt_fill_u32", "vmt_fill_f32", "vmt_fill_f64", "vmt_checksum_xor",
+    "vmt_skip", "vmt_synchronize", "vmt_export_state", "vmt_batch_fill_u32", "vmt_jump_states", "vmt_seed_states",
+    "vmt_jump_poly", "vmt_jump_poly_pow2", "vmt_charpoly", "vmt_set_tuning", "vmt_set_profiling", "vmt_last_timings", "vmt_stats",
+    "vmt_status_string", "vmt_last_error", "vmt_version",
+]
+
+
+class VmtError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+class InvalidArgument(VmtError, ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class LogicError(VmtError):
+    """std::logic_error in the reference (cadence / boundary)."""
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2309_16682_b200.build` "
+            "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    c = ctypes
+    H = c.c_void_p
+    u32p, u64p = c.POINTER(c.c_uint32), c.POINTER(c.c_uint64)
+    sig = {
+        "vmt_full_period_exponent": (c.c_uint, [c.c_uint]),
+        "vmt_create": (c.c_int, [c.c_uint32, c.c_uint, c.c_uint, c.c_int, c.POINTER(H)]),
+        "vmt_create_from_states": (c.c_int, [c.c_void_p, c.c_uint, c.c_int, c.POINTER(H)]),
+        "vmt_destroy": (c.c_int, [H]),
+        "vmt_lanes": (c.c_uint, [H]),
+        "vmt_state_words": (c.c_uint64, [H]),
+        "vmt_jump_exponent": (c.c_uint, [H]),
+        "vmt_position": (c.c_uint64, [H]),
+        "vmt_next_u32": (c.c_int, [H, u32p]),
+        "vmt_next_block16": (c.c_int, [H, c.c_void_p]),
+        "vmt_next_block_state": (c.c_int, [H, c.c_void_p]),
+        "vmt_fill_u32": (c.c_int, [H, c.c_void_p, c.c_uint64, c.c_void_p]),
+        "vmt_fill_f32": (c.c_int, [H, c.c_void_p, c.c_uint64, c.c_int, c.c_void_p]),
+        "vmt_fill_f64": (c.c_int, [H, c.c_void_p, c.c_uint64, c.c_int, c.c_void_p]),
+        "vmt_checksum_xor": (c.c_int, [H, c.c_uint64, u32p, c.c_void_p]),
+        "vmt_skip": (c.c_int, [H, c.c_uint64]),
+        "vmt_synchronize": (c.c_int, [H]),
+        "vmt_export_state": (c.c_int, [H, c.c_void_p]),
+        "vmt_batch_fill_u32": (c.c_int, [c.c_uint32, c.c_uint, c.c_uint, c.c_uint, c.c_uint64, c.c_void_p,
+                                         c.c_int, c.c_void_p]),
+        "vmt_jump_states": (c.c_int, [c.c_void_p, c.c_uint64, c.c_void_p, c.c_void_p, c.c_int, c.c_void_p]),
+        "vmt_seed_states": (c.c_int, [c.c_void_p, c.c_uint64, c.c_void_p, c.c_int, c.c_void_p]),
+        "vmt_jump_poly": (c.c_int, [c.c_uint64, c.c_uint64, c.c_void_p]),
+        "vmt_jump_poly_pow2": (c.c_int, [c.c_uint, c.c_void_p]),
+        "vmt_charpoly": (c.c_int, [c.c_void_p]),
+        "vmt_set_tuning": (c.c_int, [H, c.c_uint, c.c_int]),
+        "vmt_stats": (c.c_int, [H, u64p, u64p, u64p, u64p]),
+        "vmt_set_profiling": (c.c_int, [H, c.c_int]),
+        "vmt_last_timings": (c.c_int, [H, c.POINTER(c.c_float), c.POINTER(c.c_float)]),
+        "vmt_status_string": (c.c_char_p, [c.c_int]),
+        "vmt_last_error": (c.c_char_p, []),
+        "vmt_version": (c.c_int, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def check(rc: int) -> None:
+    if rc == VMT_OK:
+        return
+    msg = (lib.vmt_last_error() or b"").decode(errors="replace")
+    if rc == VMT_EINVAL:
+        raise InvalidArgument(rc, msg)
+    if rc == VMT_ESTATE:
+        raise LogicError(rc, msg)
+    raise VmtError(rc, msg)

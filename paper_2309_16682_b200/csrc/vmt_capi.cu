@@ -1,0 +1,1158 @@
+// C ABI of the B200-native VMT19937 generator (include/vmt19937_b200.h).
+//
+// Host runtime: positions, chunk planning, jump-polynomial caches and
+// staging; every word is produced by the sm_100a kernels in vmt_kernels.cuh.
+// There is no CPU generation path: without a CUDA device every call that
+// produces words fails with VMT_ECUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/vmt19937_b200.h"
+#include "gf2poly.hpp"
+#include "vmt_kernels.cuh"
+
+using namespace vmt_b200;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct VmtError : std::runtime_error {
+    int code;
+    VmtError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define VMT_CUDA(x)                                                                                   \
+    do {                                                                                              \
+        cudaError_t e_ = (x);                                                                         \
+        if (e_ != cudaSuccess)                                                                        \
+            throw VmtError(VMT_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));               \
+    } while (0)
+
+void require(bool c, int code, const char* msg) {
+    if (!c)
+        throw VmtError(code, msg);
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return VMT_OK;
+    } catch (const VmtError& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "out of host memory";
+        return VMT_ENOMEM;
+    } catch (const std::invalid_argument& e) {
+        g_last_error = e.what();
+        return VMT_EINVAL;
+    } catch (const std::logic_error& e) {
+        g_last_error = e.what();
+        return VMT_ESTATE;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return VMT_EIO;
+    }
+}
+
+bool valid_lanes(unsigned L) { return L == 1 || L == 2 || L == 4 || L == 8 || L == 16 || L == 32; }
+
+unsigned log2u(unsigned L) {
+    unsigned r = 0;
+    while ((1u << r) < L)
+        ++r;
+    return r;
+}
+
+// ---------------------------------------------------------------- kernels --
+using GenFn = void (*)(GenParams);
+
+struct Variant {
+    int L = 0, R = 0, NT = 0, SMEM = 0;
+    GenFn fn[6][2] = {};
+};
+
+template <int L, int R, int MODE>
+void fill_mode(Variant& v) {
+    v.fn[MODE][0] = vmt_gen_kernel<L, R, MODE, false>;
+    v.fn[MODE][1] = vmt_gen_kernel<L, R, MODE, true>;
+}
+
+template <int L, int R>
+Variant make_variant() {
+    Variant v;
+    v.L = L;
+    v.R = R;
+    v.NT = GenShape<L, R>::NT;
+    v.SMEM = GenShape<L, R>::SMEM;
+    fill_mode<L, R, MODE_U32>(v);
+    fill_mode<L, R, MODE_XOR>(v);
+    fill_mode<L, R, MODE_F32>(v);
+    fill_mode<L, R, MODE_F64>(v);
+    fill_mode<L, R, MODE_F64_REAL3>(v);
+    fill_mode<L, R, MODE_F64_RES53>(v);
+    return v;
+}
+
+// variant ids: 0 auto; 1 R=13; 2 R=4; 3 R=2; 4 R=8; 5 R=1 (run length R =
+// consecutive words per thread per window; see GenShape)
+int run_length_of(int variant) {
+    switch (variant) {
+    case 1: return 13;
+    case 2: return 4;
+    case 3: return 2;
+    case 4: return 8;
+    case 5: return 1;
+    default: return -1;
+    }
+}
+
+const Variant& pick_variant(unsigned L, int variant) {
+    static const Variant v32[] = {make_variant<32, 13>(), make_variant<32, 4>(), make_variant<32, 2>(),
+                                  make_variant<32, 8>()};
+    static const Variant v16[] = {make_variant<16, 13>(), make_variant<16, 4>(), make_variant<16, 2>(),
+                                  make_variant<16, 1>()};
+    static const Variant v8[] = {make_variant<8, 13>(), make_variant<8, 4>(), make_variant<8, 2>(),
+                                 make_variant<8, 1>()};
+    static const Variant v4[] = {make_variant<4, 4>(), make_variant<4, 1>()};
+    static const Variant v2 = make_variant<2, 1>(), v1 = make_variant<1, 1>();
+    auto find = [&](const Variant* vs, int n, int R) -> const Variant& {
+        for (int i = 0; i < n; ++i)
+            if (vs[i].R == R)
+                return vs[i];
+        throw VmtError(VMT_EINVAL, "unknown kernel variant for this lane count");
+    };
+    const int R = run_length_of(variant);
+    switch (L) {
+    case 32: return find(v32, 4, variant == 0 ? 2 : R);
+    case 16: return find(v16, 4, variant == 0 ? 1 : R);
+    case 8: return find(v8, 4, variant == 0 ? 1 : R);
+    case 4: return find(v4, 2, variant == 0 ? 1 : R);
+    case 2:
+        if (variant != 0 && R != 1)
+            throw VmtError(VMT_EINVAL, "unknown kernel variant for this lane count");
+        return v2;
+    case 1:
+        if (variant != 0 && R != 1)
+            throw VmtError(VMT_EINVAL, "unknown kernel variant for this lane count");
+        return v1;
+    default: throw VmtError(VMT_EINVAL, "lanes must be one of 1, 2, 4, 8, 16, 32");
+    }
+}
+
+struct DeviceInfo {
+    int sms = 0;
+    std::set<const void*> smem_set;
+    std::map<const void*, int> occ;
+};
+std::mutex g_dev_mu;
+std::map<int, DeviceInfo> g_dev;
+
+DeviceInfo& device_info(int dev) {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    auto& d = g_dev[dev];
+    if (d.sms == 0) {
+        VMT_CUDA(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return d;
+}
+
+// Occupancy (CTAs per SM) of a generation kernel, opting into >48 KB smem.
+int prepare_gen(int dev, GenFn fn, int nt, int smem) {
+    DeviceInfo& d = device_info(dev);
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    const void* key = reinterpret_cast<const void*>(fn);
+    if (!d.smem_set.count(key)) {
+        VMT_CUDA(cudaFuncSetAttribute(key, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        int occ = 0;
+        VMT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, key, nt, smem));
+        d.occ[key] = std::max(occ, 1);
+        d.smem_set.insert(key);
+    }
+    return d.occ[key];
+}
+
+// ------------------------------------------------------- device buffers --
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t cap = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    void swap(DevBuf& o) {
+        std::swap(p, o.p);
+        std::swap(cap, o.cap);
+    }
+    void reserve(size_t n) {
+        if (n <= cap)
+            return;
+        if (p)
+            cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        VMT_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+        cap = n;
+    }
+    ~DevBuf() {
+        if (p)
+            cudaFree(p);
+    }
+};
+
+// ------------------------------------------------------------ polynomials --
+// J^1..J^(n) for J = x^(624*blocks): the chunk-start jump polynomials.
+struct PolySet {
+    std::vector<Poly> host;
+    DevBuf<std::uint64_t> dev;
+    size_t dev_count = 0;
+};
+
+void powers_parallel(const Poly& J, size_t count, std::vector<Poly>& out, size_t have) {
+    // out[c-1] = J^c for c = have+1 .. count
+    Gf2Field& F = Gf2Field::instance();
+    if (out.size() < count)
+        out.resize(count);
+    if (have >= count)
+        return;
+    const size_t todo = count - have;
+    unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 16u));
+    nt = (unsigned)std::min<size_t>(nt, (todo + 7) / 8);
+    std::vector<std::thread> th;
+    for (unsigned k = 0; k < nt; ++k) {
+        const size_t lo = have + 1 + todo * k / nt, hi = have + todo * (k + 1) / nt; // inclusive range
+        th.emplace_back([&, lo, hi] {
+            if (lo > hi)
+                return;
+            Poly cur = (lo - 1 >= 1 && lo - 1 <= have) ? out[lo - 2] : F.powmod(J, lo - 1);
+            if (lo - 1 == 0)
+                cur = F.one();
+            for (size_t c = lo; c <= hi; ++c) {
+                cur = F.mulmod(cur, J);
+                out[c - 1] = cur;
+            }
+        });
+    }
+    for (auto& t : th)
+        t.join();
+}
+
+std::mutex g_poly_mu;
+
+// 8-bit digit tables T_j[v] = x^(v * 2^(8j)), j < 8, v < 256 (config 5 jumps).
+struct DigitTables {
+    std::vector<Poly> host; // index j*256 + v (v=0 unused)
+    std::map<int, std::unique_ptr<DevBuf<std::uint64_t>>> dev;
+};
+DigitTables& digit_tables() {
+    static DigitTables t;
+    std::lock_guard<std::mutex> lk(g_poly_mu);
+    if (t.host.empty()) {
+        Gf2Field& F = Gf2Field::instance();
+        t.host.assign(8 * 256, Poly(kPolyWords, 0));
+        std::vector<std::thread> th;
+        for (int j = 0; j < 8; ++j)
+            th.emplace_back([&, j] {
+                const Poly base = F.x_pow2(8 * j);
+                Poly cur = F.one();
+                t.host[j * 256] = cur;
+                for (int v = 1; v < 256; ++v) {
+                    cur = F.mulmod(cur, base);
+                    t.host[j * 256 + v] = cur;
+                }
+            });
+        for (auto& x : th)
+            x.join();
+    }
+    return t;
+}
+
+const std::uint64_t* digit_tables_device(int dev) {
+    DigitTables& t = digit_tables();
+    std::lock_guard<std::mutex> lk(g_poly_mu);
+    auto& slot = t.dev[dev];
+    if (!slot) {
+        slot.reset(new DevBuf<std::uint64_t>());
+        slot->reserve(t.host.size() * kPolyWords);
+        std::vector<std::uint64_t> flat(t.host.size() * kPolyWords);
+        for (size_t i = 0; i < t.host.size(); ++i)
+            std::memcpy(flat.data() + i * kPolyWords, t.host[i].data(), kPolyWords * 8);
+        VMT_CUDA(cudaMemcpy(slot->p, flat.data(), flat.size() * 8, cudaMemcpyHostToDevice));
+    }
+    return slot->p;
+}
+
+// Dephasing polynomials x^(t*2^q) mod P, t = 1..L-1.
+std::vector<Poly> dephase_polys(unsigned q, unsigned L) {
+    Gf2Field& F = Gf2Field::instance();
+    std::vector<Poly> out;
+    if (L <= 1)
+        return out;
+    const Poly base = F.x_pow2(q);
+    Poly cur = base;
+    out.push_back(cur);
+    for (unsigned t = 2; t < L; ++t) {
+        cur = F.mulmod(cur, base);
+        out.push_back(cur);
+    }
+    return out;
+}
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a{};
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+struct Counters {
+    std::uint64_t gen = 0, jump = 0, other = 0, lane_jumps = 0;
+};
+
+// Launches the jump kernel on jobs (all host vectors; uploaded to dev scratch).
+void launch_jumps(cudaStream_t st, const std::uint32_t* src, int src_stride, std::uint32_t* dst, int dst_stride,
+                  const std::uint64_t* d_polys, const std::vector<long long>& jsrc,
+                  const std::vector<long long>& jdst, const std::vector<int>& jpoly, DevBuf<long long>& dsrc,
+                  DevBuf<long long>& ddst, DevBuf<int>& dpoly, Counters& cnt) {
+    const int n = (int)jsrc.size();
+    if (n == 0)
+        return;
+    dsrc.reserve(n);
+    ddst.reserve(n);
+    dpoly.reserve(n);
+    VMT_CUDA(cudaMemcpyAsync(dsrc.p, jsrc.data(), n * sizeof(long long), cudaMemcpyHostToDevice, st));
+    VMT_CUDA(cudaMemcpyAsync(ddst.p, jdst.data(), n * sizeof(long long), cudaMemcpyHostToDevice, st));
+    VMT_CUDA(cudaMemcpyAsync(dpoly.p, jpoly.data(), n * sizeof(int), cudaMemcpyHostToDevice, st));
+    JumpParams jp{};
+    jp.src = src;
+    jp.dst = dst;
+    jp.polys = d_polys;
+    jp.job_src = dsrc.p;
+    jp.job_dst = ddst.p;
+    jp.job_poly = dpoly.p;
+    jp.src_stride = src_stride;
+    jp.dst_stride = dst_stride;
+    jp.njobs = n;
+    vmt_jump_kernel<<<(n + kJumpWarps - 1) / kJumpWarps, kJumpWarps * 32, 0, st>>>(jp);
+    VMT_CUDA(cudaGetLastError());
+    cnt.jump += 1;
+    cnt.lane_jumps += n;
+    // the job tables are host vectors owned by the caller; make the upload
+    // complete before they can be released
+    VMT_CUDA(cudaStreamSynchronize(st));
+}
+
+struct AffineJobs {
+    int n = 0, div = 1;
+    long long s_a = 0, s_b = 0, s_c = 0, d_a = 0, d_b = 0, d_c = 0;
+    int p_a = 0, p_b = 0, p_c = 0;
+};
+
+// Launches the jump kernel with jobs given by an affine map of the job index
+// (no host tables, fully asynchronous).
+void launch_jumps_affine(cudaStream_t st, const std::uint32_t* src, int src_stride, std::uint32_t* dst,
+                         int dst_stride, const std::uint64_t* d_polys, const AffineJobs& a, Counters& cnt) {
+    if (a.n == 0)
+        return;
+    JumpParams jp{};
+    jp.src = src;
+    jp.dst = dst;
+    jp.polys = d_polys;
+    jp.src_stride = src_stride;
+    jp.dst_stride = dst_stride;
+    jp.njobs = a.n;
+    jp.div = a.div;
+    jp.s_a = a.s_a;
+    jp.s_b = a.s_b;
+    jp.s_c = a.s_c;
+    jp.d_a = a.d_a;
+    jp.d_b = a.d_b;
+    jp.d_c = a.d_c;
+    jp.p_a = a.p_a;
+    jp.p_b = a.p_b;
+    jp.p_c = a.p_c;
+    vmt_jump_kernel<<<(a.n + kJumpWarps - 1) / kJumpWarps, kJumpWarps * 32, 0, st>>>(jp);
+    VMT_CUDA(cudaGetLastError());
+    cnt.jump += 1;
+    cnt.lane_jumps += a.n;
+}
+
+} // namespace
+
+// ------------------------------------------------------------------ handle --
+struct vmt_generator {
+    int device = 0;
+    unsigned L = 1;
+    unsigned q = 0;
+    std::uint64_t bw = 624;
+    cudaStream_t own = nullptr;
+    cudaEvent_t last = nullptr;
+    cudaStream_t last_stream = nullptr;
+
+    DevBuf<std::uint32_t> base;   // [624][L] boundary states at block 0
+    DevBuf<std::uint32_t> cur;    // [624][L] at cur_block
+    DevBuf<std::uint32_t> next;   // save target
+    std::uint64_t cur_block = 0;
+    std::uint64_t pos = 0;  // words consumed by the caller
+    std::uint64_t gpos = 0; // words produced by the GPU (>= pos)
+
+    DevBuf<std::uint32_t> chunks;    // [C][624][L]
+    DevBuf<std::uint32_t> partials;  // per-CTA xor partials
+    DevBuf<std::uint32_t> scratch;   // device staging for host destinations
+    DevBuf<std::uint64_t> tmp_poly;
+    DevBuf<long long> jsrc, jdst;
+    DevBuf<int> jpoly;
+    std::uint32_t* hstage = nullptr; // pinned staging for single / block16 queries
+    std::uint64_t hstage_cap = 0, hstage_start = 0;
+    std::uint32_t* hsmall = nullptr; // pinned 4-byte readback
+
+    std::map<std::uint64_t, std::unique_ptr<PolySet>> polycache; // blocks-per-chunk -> J^c
+    unsigned max_chunks = 0;
+    int variant = 0;
+    Counters cnt;
+    bool profile = false;
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr}; // before jumps, before gen, after gen
+    bool ev_valid = false;
+
+    cudaStream_t pick(void* s) {
+        cudaStream_t st = s ? static_cast<cudaStream_t>(s) : own;
+        if (last_stream && st != last_stream)
+            VMT_CUDA(cudaStreamWaitEvent(st, last, 0));
+        return st;
+    }
+    void mark(cudaStream_t st) {
+        VMT_CUDA(cudaEventRecord(last, st));
+        last_stream = st;
+    }
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        VMT_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        if (prev >= 0)
+            cudaSetDevice(prev);
+    }
+};
+
+void check_device(int device) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        throw VmtError(VMT_ECUDA, "no CUDA device available (the generator has no CPU path)");
+    }
+    require(device >= 0 && device < n, VMT_EINVAL, "device ordinal out of range");
+}
+
+const std::uint64_t* upload_polys(vmt_generator* h, const std::vector<Poly>& polys, cudaStream_t st) {
+    h->tmp_poly.reserve(std::max<size_t>(polys.size(), 1) * kPolyWords);
+    std::vector<std::uint64_t> flat(polys.size() * kPolyWords);
+    for (size_t i = 0; i < polys.size(); ++i)
+        std::memcpy(flat.data() + i * kPolyWords, polys[i].data(), kPolyWords * 8);
+    VMT_CUDA(cudaMemcpyAsync(h->tmp_poly.p, flat.data(), flat.size() * 8, cudaMemcpyHostToDevice, st));
+    VMT_CUDA(cudaStreamSynchronize(st));
+    return h->tmp_poly.p;
+}
+
+// Chunk-start polynomials J^1..J^(C-1) for B blocks per chunk (cached).
+const std::uint64_t* chunk_polys(vmt_generator* h, std::uint64_t B, size_t C, cudaStream_t st) {
+    auto& slot = h->polycache[B];
+    if (!slot)
+        slot.reset(new PolySet());
+    PolySet& ps = *slot;
+    const size_t need = C > 0 ? C - 1 : 0;
+    if (ps.host.size() < need) {
+        Gf2Field& F = Gf2Field::instance();
+        const Poly J = F.x_pow(624ull * B);
+        const size_t have = ps.host.size();
+        powers_parallel(J, need, ps.host, have);
+    }
+    if (ps.dev_count < need) {
+        ps.dev.reserve(need * kPolyWords);
+        std::vector<std::uint64_t> flat(need * kPolyWords);
+        for (size_t i = 0; i < need; ++i)
+            std::memcpy(flat.data() + i * kPolyWords, ps.host[i].data(), kPolyWords * 8);
+        VMT_CUDA(cudaMemcpyAsync(ps.dev.p, flat.data(), flat.size() * 8, cudaMemcpyHostToDevice, st));
+        VMT_CUDA(cudaStreamSynchronize(st));
+        ps.dev_count = need;
+    }
+    return ps.dev.p;
+}
+
+// Moves h->cur (block cur_block) to block `target` (>= cur_block) by one jump.
+void reposition(vmt_generator* h, std::uint64_t target, cudaStream_t st) {
+    if (target == h->cur_block)
+        return;
+    const std::uint32_t* from = h->cur.p;
+    std::uint64_t delta = 0;
+    if (target > h->cur_block) {
+        delta = target - h->cur_block;
+    } else {
+        from = h->base.p;
+        delta = target;
+    }
+    Gf2Field& F = Gf2Field::instance();
+    // 624*delta may exceed 64 bits for huge skips
+    const unsigned __int128 d = (unsigned __int128)624u * delta;
+    std::vector<Poly> polys{F.x_pow128((std::uint64_t)d, (std::uint64_t)(d >> 64))};
+    const std::uint64_t* dp = upload_polys(h, polys, st);
+    AffineJobs a;
+    a.n = (int)h->L;
+    a.div = (int)h->L;
+    a.s_b = 1;
+    a.d_b = 1;
+    launch_jumps_affine(st, from, (int)h->L, h->next.p, (int)h->L, dp, a, h->cnt);
+    h->cur.swap(h->next);
+    h->cur_block = target;
+}
+
+// Core: GPU-produces stream words [h->gpos, h->gpos + n) into `out` in the
+// representation of `mode` (out == nullptr only for MODE_XOR). Advances gpos.
+void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaStream_t st, std::uint32_t* xor_out_dev) {
+    if (n == 0)
+        return;
+    const std::uint64_t P0 = h->gpos, P1 = h->gpos + n;
+    const std::uint64_t b0 = P0 / h->bw, b1 = (P1 + h->bw - 1) / h->bw;
+    reposition(h, b0, st);
+    if (h->profile)
+        VMT_CUDA(cudaEventRecord(h->ev[0], st));
+    const Variant& v = pick_variant(h->L, h->variant);
+    const int groups = 1; // a CTA holds all L lanes of its chunk
+    const std::uint64_t nb = b1 - b0;
+    // VEC when the destination is aligned for the vector width: the element
+    // of stream word g lives at out + (g - P0).
+    const int esz = (mode == MODE_U32 || mode == MODE_F32 || mode == MODE_XOR) ? 4 : 8;
+    bool vec = false;
+    if (mode != MODE_XOR && mode != MODE_F64_RES53) {
+        const int V = v.L >= 4 ? 4 : v.L;
+        const std::uintptr_t a = reinterpret_cast<std::uintptr_t>(out);
+        const std::uint64_t e = (std::uint64_t)(a / (std::uintptr_t)esz);
+        const int need = (esz == 8) ? 2 : V; // double2 / VecT<V> stores
+        vec = (a % (std::uintptr_t)esz == 0) && ((e - P0) % (std::uint64_t)need == 0) && (P0 % V == 0) &&
+              (esz == 4 || V == 4);
+    }
+    GenFn fn = v.fn[mode][vec ? 1 : 0];
+    const int occ = prepare_gen(h->device, fn, v.NT, v.SMEM);
+    const int sms = device_info(h->device).sms;
+    const std::uint64_t max_grid = (std::uint64_t)sms * occ;
+    std::uint64_t C = std::max<std::uint64_t>(1, max_grid / groups);
+    if (h->max_chunks)
+        C = std::min<std::uint64_t>(C, h->max_chunks);
+    C = std::min<std::uint64_t>(C, nb);
+    const std::uint64_t B = (nb + C - 1) / C;
+    C = (nb + B - 1) / B;
+
+    h->chunks.reserve((size_t)C * kN * h->L);
+    VMT_CUDA(cudaMemcpyAsync(h->chunks.p, h->cur.p, (size_t)kN * h->L * 4, cudaMemcpyDeviceToDevice, st));
+    if (C > 1) {
+        const std::uint64_t* dp = chunk_polys(h, B, C, st);
+        AffineJobs a;
+        a.n = (int)((C - 1) * h->L);
+        a.div = (int)h->L;
+        a.s_b = 1;
+        a.d_a = (long long)kN * h->L;
+        a.d_b = 1;
+        a.d_c = (long long)kN * h->L;
+        a.p_a = 1;
+        launch_jumps_affine(st, h->cur.p, (int)h->L, h->chunks.p, (int)h->L, dp, a, h->cnt);
+    }
+    const std::uint64_t grid = C * groups;
+    if (h->profile)
+        VMT_CUDA(cudaEventRecord(h->ev[1], st));
+    if (mode == MODE_XOR)
+        h->partials.reserve(grid);
+    GenParams p{};
+    p.chunk_states = h->chunks.p;
+    p.out = out;
+    p.xor_partials = h->partials.p;
+    p.save_state = h->next.p;
+    p.first_block = b0;
+    p.end_block = b1;
+    p.pos_begin = P0;
+    p.pos_end = P1;
+    p.save_block = P1 / h->bw;
+    p.out_chunk_stride = 0;
+    p.blocks_per_chunk = (unsigned)B;
+    p.lanes = h->L;
+    fn<<<(unsigned)grid, v.NT, v.SMEM, st>>>(p);
+    VMT_CUDA(cudaGetLastError());
+    h->cnt.gen += 1;
+    if (h->profile) {
+        VMT_CUDA(cudaEventRecord(h->ev[2], st));
+        h->ev_valid = true;
+    }
+    if (mode == MODE_XOR) {
+        vmt_xor_reduce_kernel<<<1, 256, 0, st>>>(h->partials.p, (int)grid, xor_out_dev);
+        VMT_CUDA(cudaGetLastError());
+        h->cnt.other += 1;
+    }
+    h->cur.swap(h->next);
+    h->cur_block = P1 / h->bw;
+    h->gpos = P1;
+}
+
+// Serves words [pos, pos+take) from the host staging buffer into dst.
+std::uint64_t drain_stage(vmt_generator* h, void* dst, int mode, std::uint64_t n, bool dst_dev, cudaStream_t st) {
+    if (h->pos >= h->gpos || mode != MODE_U32)
+        return 0;
+    const std::uint64_t take = std::min<std::uint64_t>(n, h->gpos - h->pos);
+    const std::uint32_t* src = h->hstage + (h->pos - h->hstage_start);
+    if (dst_dev)
+        VMT_CUDA(cudaMemcpyAsync(dst, src, take * 4, cudaMemcpyHostToDevice, st));
+    else
+        std::memcpy(dst, src, take * 4);
+    h->pos += take;
+    return take;
+}
+
+void fill_generic(vmt_generator* h, void* dst, std::uint64_t n, int mode, void* stream) {
+    require(dst != nullptr || n == 0, VMT_EINVAL, "null destination");
+    if (n == 0)
+        return;
+    DeviceGuard g(h->device);
+    cudaStream_t st = h->pick(stream);
+    const bool dev = is_device_ptr(dst);
+    std::uint64_t words = (mode == MODE_F64_RES53) ? 2 * n : n;
+    if (h->pos < h->gpos) {
+        require(mode == MODE_U32 || mode == MODE_XOR, VMT_ESTATE,
+                "conversion fills cannot resume inside a partially consumed single-query buffer");
+        const std::uint64_t took = drain_stage(h, dst, mode, n, dev, st);
+        dst = static_cast<std::uint32_t*>(dst) + took;
+        words -= took;
+        n -= took;
+    }
+    if (words == 0) {
+        h->mark(st);
+        return;
+    }
+    require(mode != MODE_F64_RES53 || (h->gpos % 2) == 0, VMT_ESTATE, "RES53 needs an even stream position");
+    const int esz = (mode == MODE_F64 || mode == MODE_F64_REAL3 || mode == MODE_F64_RES53) ? 8 : 4;
+    if (dev) {
+        gpu_generate(h, mode, dst, words, st, nullptr);
+    } else {
+        const std::uint64_t bytes = n * (std::uint64_t)esz;
+        h->scratch.reserve((bytes + 3) / 4 + 4);
+        gpu_generate(h, mode, h->scratch.p, words, st, nullptr);
+        VMT_CUDA(cudaMemcpyAsync(dst, h->scratch.p, bytes, cudaMemcpyDeviceToHost, st));
+        VMT_CUDA(cudaStreamSynchronize(st));
+    }
+    h->pos = h->gpos;
+    h->mark(st);
+}
+
+void refill_stage(vmt_generator* h) {
+    DeviceGuard g(h->device);
+    cudaStream_t st = h->pick(nullptr);
+    const std::uint64_t S = std::max<std::uint64_t>(h->bw, 1u << 16);
+    if (h->hstage_cap < S) {
+        if (h->hstage)
+            cudaFreeHost(h->hstage);
+        h->hstage = nullptr;
+        VMT_CUDA(cudaMallocHost(&h->hstage, S * 4));
+        h->hstage_cap = S;
+    }
+    h->scratch.reserve(S);
+    h->hstage_start = h->gpos;
+    gpu_generate(h, MODE_U32, h->scratch.p, S, st, nullptr);
+    VMT_CUDA(cudaMemcpyAsync(h->hstage, h->scratch.p, S * 4, cudaMemcpyDeviceToHost, st));
+    VMT_CUDA(cudaStreamSynchronize(st));
+    h->mark(st);
+}
+
+// Builds interleaved [624][L] de-phased states for `ngen` generators with
+// seeds seed0.. into dst (generator stride 624*L words).
+void build_dephased(int device, cudaStream_t st, std::uint32_t seed0, unsigned ngen, unsigned L, unsigned q,
+                    std::uint32_t* dst, DevBuf<std::uint64_t>& polybuf, Counters& cnt) {
+    std::vector<std::uint32_t> seeds(ngen);
+    for (unsigned g = 0; g < ngen; ++g)
+        seeds[g] = seed0 + g;
+    DevBuf<std::uint32_t> dseeds;
+    dseeds.reserve(ngen);
+    VMT_CUDA(cudaMemcpyAsync(dseeds.p, seeds.data(), ngen * 4, cudaMemcpyHostToDevice, st));
+    vmt_seed_kernel<<<(ngen + 127) / 128, 128, 0, st>>>(dseeds.p, (int)ngen, dst, (long long)kN * L, (int)L);
+    VMT_CUDA(cudaGetLastError());
+    cnt.other += 1;
+    if (L > 1) {
+        const std::vector<Poly> polys = dephase_polys(q, L);
+        polybuf.reserve(polys.size() * kPolyWords);
+        std::vector<std::uint64_t> flat(polys.size() * kPolyWords);
+        for (size_t i = 0; i < polys.size(); ++i)
+            std::memcpy(flat.data() + i * kPolyWords, polys[i].data(), kPolyWords * 8);
+        VMT_CUDA(cudaMemcpyAsync(polybuf.p, flat.data(), flat.size() * 8, cudaMemcpyHostToDevice, st));
+        AffineJobs a;
+        a.n = (int)(ngen * (L - 1));
+        a.div = (int)(L - 1);
+        a.s_a = (long long)kN * L;
+        a.d_a = (long long)kN * L;
+        a.d_b = 1;
+        a.d_c = 1;
+        a.p_b = 1;
+        launch_jumps_affine(st, dst, (int)L, dst, (int)L, polybuf.p, a, cnt);
+    }
+    VMT_CUDA(cudaStreamSynchronize(st));
+}
+
+vmt_generator* new_handle(unsigned L, int device) {
+    check_device(device);
+    auto* h = new vmt_generator();
+    h->device = device;
+    h->L = L;
+    h->bw = 624ull * L;
+    DeviceGuard g(device);
+    VMT_CUDA(cudaStreamCreateWithFlags(&h->own, cudaStreamNonBlocking));
+    VMT_CUDA(cudaEventCreateWithFlags(&h->last, cudaEventDisableTiming));
+    h->base.reserve((size_t)kN * L);
+    h->cur.reserve((size_t)kN * L);
+    h->next.reserve((size_t)kN * L);
+    VMT_CUDA(cudaMallocHost(&h->hsmall, 64));
+    return h;
+}
+
+} // namespace
+
+// =================================================================== C ABI ==
+extern "C" {
+
+unsigned vmt_full_period_exponent(unsigned lanes) { return unsigned(kDeg) - log2u(lanes ? lanes : 1); }
+
+int vmt_create(uint32_t seed, unsigned lanes, unsigned jump_exponent, int device, vmt_handle* out) {
+    return guarded([&] {
+        require(out != nullptr, VMT_EINVAL, "null handle pointer");
+        require(valid_lanes(lanes), VMT_EINVAL, "lanes must be one of 1, 2, 4, 8, 16, 32");
+        const unsigned q = jump_exponent == VMT_FULL_PERIOD ? vmt_full_period_exponent(lanes) : jump_exponent;
+        std::unique_ptr<vmt_generator> h(new_handle(lanes, device));
+        h->q = q;
+        DeviceGuard g(device);
+        build_dephased(device, h->own, seed, 1, lanes, q, h->base.p, h->tmp_poly, h->cnt);
+        VMT_CUDA(cudaMemcpyAsync(h->cur.p, h->base.p, (size_t)kN * lanes * 4, cudaMemcpyDeviceToDevice, h->own));
+        VMT_CUDA(cudaStreamSynchronize(h->own));
+        *out = h.release();
+    });
+}
+
+int vmt_create_from_states(const uint32_t* lane_states, unsigned lanes, int device, vmt_handle* out) {
+    return guarded([&] {
+        require(out != nullptr && lane_states != nullptr, VMT_EINVAL, "null pointer");
+        require(valid_lanes(lanes), VMT_EINVAL, "lanes must be one of 1, 2, 4, 8, 16, 32");
+        std::unique_ptr<vmt_generator> h(new_handle(lanes, device));
+        h->q = 0;
+        std::vector<std::uint32_t> il((size_t)kN * lanes), ls((size_t)kN * lanes);
+        if (is_device_ptr(lane_states))
+            VMT_CUDA(cudaMemcpy(ls.data(), lane_states, ls.size() * 4, cudaMemcpyDeviceToHost));
+        else
+            std::memcpy(ls.data(), lane_states, ls.size() * 4);
+        for (unsigned k = 0; k < (unsigned)kN; ++k)
+            for (unsigned t = 0; t < lanes; ++t)
+                il[(size_t)k * lanes + t] = ls[(size_t)t * kN + k];
+        DeviceGuard g(device);
+        VMT_CUDA(cudaMemcpy(h->base.p, il.data(), il.size() * 4, cudaMemcpyHostToDevice));
+        VMT_CUDA(cudaMemcpy(h->cur.p, il.data(), il.size() * 4, cudaMemcpyHostToDevice));
+        *out = h.release();
+    });
+}
+
+int vmt_destroy(vmt_handle h) {
+    return guarded([&] {
+        if (!h)
+            return;
+        {
+            DeviceGuard g(h->device);
+            cudaStreamSynchronize(h->own);
+            if (h->hstage)
+                cudaFreeHost(h->hstage);
+            if (h->hsmall)
+                cudaFreeHost(h->hsmall);
+            cudaEventDestroy(h->last);
+            for (auto& e : h->ev)
+                if (e)
+                    cudaEventDestroy(e);
+            cudaStreamDestroy(h->own);
+            delete h;
+        }
+    });
+}
+
+unsigned vmt_lanes(vmt_handle h) { return h ? h->L : 0; }
+uint64_t vmt_state_words(vmt_handle h) { return h ? h->bw : 0; }
+unsigned vmt_jump_exponent(vmt_handle h) { return h ? h->q : 0; }
+uint64_t vmt_position(vmt_handle h) { return h ? h->pos : 0; }
+
+int vmt_next_u32(vmt_handle h, uint32_t* out) {
+    return guarded([&] {
+        require(h && out, VMT_EINVAL, "null argument");
+        if (h->pos >= h->gpos)
+            refill_stage(h);
+        *out = h->hstage[h->pos - h->hstage_start];
+        ++h->pos;
+    });
+}
+
+int vmt_next_block16(vmt_handle h, uint32_t* out16) {
+    return guarded([&] {
+        require(h && out16, VMT_EINVAL, "null argument");
+        for (int i = 0; i < 16; ++i) {
+            if (h->pos >= h->gpos)
+                refill_stage(h);
+            out16[i] = h->hstage[h->pos - h->hstage_start];
+            ++h->pos;
+        }
+    });
+}
+
+int vmt_next_block_state(vmt_handle h, uint32_t* out) {
+    return guarded([&] {
+        require(h && out, VMT_EINVAL, "null argument");
+        if (h->pos % h->bw != 0)
+            throw VmtError(VMT_ESTATE, "state-block query off a state-block boundary");
+        fill_generic(h, out, h->bw, MODE_U32, nullptr);
+        DeviceGuard g(h->device);
+        VMT_CUDA(cudaStreamSynchronize(h->last_stream ? h->last_stream : h->own));
+    });
+}
+
+int vmt_fill_u32(vmt_handle h, uint32_t* dst, uint64_t n, void* stream) {
+    return guarded([&] {
+        require(h != nullptr, VMT_EINVAL, "null handle");
+        fill_generic(h, dst, n, MODE_U32, stream);
+    });
+}
+
+int vmt_fill_f32(vmt_handle h, float* dst, uint64_t n, int rule, void* stream) {
+    return guarded([&] {
+        require(h != nullptr, VMT_EINVAL, "null handle");
+        require(rule == VMT_F32_24, VMT_EINVAL, "unknown float32 rule");
+        fill_generic(h, dst, n, MODE_F32, stream);
+    });
+}
+
+int vmt_fill_f64(vmt_handle h, double* dst, uint64_t n, int rule, void* stream) {
+    return guarded([&] {
+        require(h != nullptr, VMT_EINVAL, "null handle");
+        int mode = 0;
+        switch (rule) {
+        case VMT_F64_32: mode = MODE_F64; break;
+        case VMT_F64_REAL3: mode = MODE_F64_REAL3; break;
+        case VMT_F64_RES53: mode = MODE_F64_RES53; break;
+        default: throw VmtError(VMT_EINVAL, "unknown float64 rule");
+        }
+        fill_generic(h, dst, n, mode, stream);
+    });
+}
+
+int vmt_checksum_xor(vmt_handle h, uint64_t n, uint32_t* out, void* stream) {
+    return guarded([&] {
+        require(h && out, VMT_EINVAL, "null argument");
+        DeviceGuard g(h->device);
+        cudaStream_t st = h->pick(stream);
+        std::uint32_t acc = 0;
+        if (h->pos < h->gpos) {
+            const std::uint64_t take = std::min<std::uint64_t>(n, h->gpos - h->pos);
+            for (std::uint64_t i = 0; i < take; ++i)
+                acc ^= h->hstage[h->pos - h->hstage_start + i];
+            h->pos += take;
+            n -= take;
+        }
+        if (n) {
+            h->scratch.reserve(4);
+            gpu_generate(h, MODE_XOR, nullptr, n, st, h->scratch.p);
+            VMT_CUDA(cudaMemcpyAsync(h->hsmall, h->scratch.p, 4, cudaMemcpyDeviceToHost, st));
+            VMT_CUDA(cudaStreamSynchronize(st));
+            acc ^= h->hsmall[0];
+            h->pos = h->gpos;
+        }
+        h->mark(st);
+        *out = acc;
+    });
+}
+
+int vmt_synchronize(vmt_handle h) {
+    return guarded([&] {
+        require(h != nullptr, VMT_EINVAL, "null handle");
+        DeviceGuard g(h->device);
+        VMT_CUDA(cudaStreamSynchronize(h->own));
+        if (h->last_stream)
+            VMT_CUDA(cudaEventSynchronize(h->last));
+    });
+}
+
+int vmt_skip(vmt_handle h, uint64_t d) {
+    return guarded([&] {
+        require(h != nullptr, VMT_EINVAL, "null handle");
+        if (h->pos + d <= h->gpos) {
+            h->pos += d;
+            return;
+        }
+        h->pos += d;
+        h->gpos = h->pos; // staging dropped; the GPU state is re-positioned lazily
+    });
+}
+
+int vmt_export_state(vmt_handle h, uint32_t* out) {
+    return guarded([&] {
+        require(h && out, VMT_EINVAL, "null argument");
+        DeviceGuard g(h->device);
+        cudaStream_t st = h->pick(nullptr);
+        // the reference's state after ceil(pos / bw) regenerations
+        const std::uint64_t tb = (h->pos + h->bw - 1) / h->bw;
+        const std::uint64_t keep_block = h->cur_block;
+        DevBuf<std::uint32_t> tmp;
+        tmp.reserve((size_t)kN * h->L);
+        if (tb == h->cur_block) {
+            VMT_CUDA(cudaMemcpyAsync(out, h->cur.p, (size_t)kN * h->L * 4, cudaMemcpyDeviceToHost, st));
+        } else {
+            // jump from the block-0 states (no change to the live position)
+            Gf2Field& F = Gf2Field::instance();
+            const unsigned __int128 d = (unsigned __int128)624u * tb;
+            std::vector<Poly> polys{F.x_pow128((std::uint64_t)d, (std::uint64_t)(d >> 64))};
+            const std::uint64_t* dp = upload_polys(h, polys, st);
+            AffineJobs a;
+            a.n = (int)h->L;
+            a.div = (int)h->L;
+            a.s_b = 1;
+            a.d_b = 1;
+            launch_jumps_affine(st, h->base.p, (int)h->L, tmp.p, (int)h->L, dp, a, h->cnt);
+            VMT_CUDA(cudaMemcpyAsync(out, tmp.p, (size_t)kN * h->L * 4, cudaMemcpyDeviceToHost, st));
+        }
+        VMT_CUDA(cudaStreamSynchronize(st));
+        (void)keep_block;
+        h->mark(st);
+    });
+}
+
+int vmt_batch_fill_u32(uint32_t seed0, unsigned ngen, unsigned lanes, unsigned jump_exponent, uint64_t n_per_gen,
+                       uint32_t* dst, int device, void* stream) {
+    return guarded([&] {
+        require(dst != nullptr || n_per_gen == 0, VMT_EINVAL, "null destination");
+        require(valid_lanes(lanes), VMT_EINVAL, "lanes must be one of 1, 2, 4, 8, 16, 32");
+        require(ngen > 0, VMT_EINVAL, "ngen must be positive");
+        check_device(device);
+        DeviceGuard g(device);
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamPerThread;
+        const unsigned q = jump_exponent == VMT_FULL_PERIOD ? vmt_full_period_exponent(lanes) : jump_exponent;
+        DevBuf<std::uint32_t> states;
+        DevBuf<std::uint64_t> polys;
+        Counters cnt;
+        states.reserve((size_t)ngen * kN * lanes);
+        build_dephased(device, st, seed0, ngen, lanes, q, states.p, polys, cnt);
+        if (n_per_gen == 0)
+            return;
+        const Variant& v = pick_variant(lanes, 0);
+        const bool dev = is_device_ptr(dst);
+        DevBuf<std::uint32_t> scratch;
+        std::uint32_t* out = dst;
+        if (!dev) {
+            scratch.reserve((size_t)ngen * n_per_gen);
+            out = scratch.p;
+        }
+        const bool vec = (reinterpret_cast<std::uintptr_t>(out) % 16 == 0) && (n_per_gen % 4 == 0);
+        GenFn fn = v.fn[MODE_U32][vec && v.L >= 4 ? 1 : 0];
+        prepare_gen(device, fn, v.NT, v.SMEM);
+        GenParams p{};
+        p.chunk_states = states.p;
+        p.out = out;
+        p.first_block = 0;
+        p.end_block = (n_per_gen + 624ull * lanes - 1) / (624ull * lanes);
+        p.pos_begin = 0;
+        p.pos_end = n_per_gen;
+        p.save_block = ~0ull;
+        p.out_chunk_stride = n_per_gen;
+        p.blocks_per_chunk = (unsigned)p.end_block;
+        p.lanes = lanes;
+        fn<<<ngen, v.NT, v.SMEM, st>>>(p);
+        VMT_CUDA(cudaGetLastError());
+        if (!dev)
+            VMT_CUDA(cudaMemcpyAsync(dst, scratch.p, (size_t)ngen * n_per_gen * 4, cudaMemcpyDeviceToHost, st));
+        VMT_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int vmt_jump_states(const uint32_t* src, uint64_t n, const uint64_t* distances, uint32_t* dst, int device,
+                    void* stream) {
+    return guarded([&] {
+        require(src && distances && dst, VMT_EINVAL, "null argument");
+        if (n == 0)
+            return;
+        check_device(device);
+        DeviceGuard g(device);
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamPerThread;
+        const std::uint64_t* tables = digit_tables_device(device);
+        DevBuf<std::uint32_t> buf;
+        buf.reserve(n * kN);
+        if (is_device_ptr(src))
+            VMT_CUDA(cudaMemcpyAsync(buf.p, src, n * kN * 4, cudaMemcpyDeviceToDevice, st));
+        else
+            VMT_CUDA(cudaMemcpyAsync(buf.p, src, n * kN * 4, cudaMemcpyHostToDevice, st));
+        std::vector<std::uint64_t> d(n);
+        if (is_device_ptr(distances))
+            VMT_CUDA(cudaMemcpy(d.data(), distances, n * 8, cudaMemcpyDeviceToHost));
+        else
+            std::memcpy(d.data(), distances, n * 8);
+        DevBuf<long long> js, jd;
+        DevBuf<int> jp;
+        Counters cnt;
+        for (int j = 0; j < 8; ++j) {
+            std::vector<long long> vs, vd;
+            std::vector<int> vp;
+            for (std::uint64_t i = 0; i < n; ++i) {
+                const unsigned digit = (unsigned)((d[i] >> (8 * j)) & 0xFF);
+                if (!digit)
+                    continue;
+                vs.push_back((long long)i * kN);
+                vd.push_back((long long)i * kN);
+                vp.push_back(j * 256 + (int)digit);
+            }
+            // in place: each warp reads its whole state before writing it
+            launch_jumps(st, buf.p, 1, buf.p, 1, tables, vs, vd, vp, js, jd, jp, cnt);
+        }
+        if (is_device_ptr(dst))
+            VMT_CUDA(cudaMemcpyAsync(dst, buf.p, n * kN * 4, cudaMemcpyDeviceToDevice, st));
+        else
+            VMT_CUDA(cudaMemcpyAsync(dst, buf.p, n * kN * 4, cudaMemcpyDeviceToHost, st));
+        VMT_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int vmt_seed_states(const uint32_t* seeds, uint64_t n, uint32_t* dst, int device, void* stream) {
+    return guarded([&] {
+        require(seeds && dst, VMT_EINVAL, "null argument");
+        if (n == 0)
+            return;
+        check_device(device);
+        DeviceGuard g(device);
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamPerThread;
+        DevBuf<std::uint32_t> ds, out;
+        ds.reserve(n);
+        if (is_device_ptr(seeds))
+            VMT_CUDA(cudaMemcpyAsync(ds.p, seeds, n * 4, cudaMemcpyDeviceToDevice, st));
+        else
+            VMT_CUDA(cudaMemcpyAsync(ds.p, seeds, n * 4, cudaMemcpyHostToDevice, st));
+        const bool dev = is_device_ptr(dst);
+        std::uint32_t* o = dst;
+        if (!dev) {
+            out.reserve(n * kN);
+            o = out.p;
+        }
+        vmt_seed_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(ds.p, (int)n, o, kN, 1);
+        VMT_CUDA(cudaGetLastError());
+        if (!dev)
+            VMT_CUDA(cudaMemcpyAsync(dst, out.p, n * kN * 4, cudaMemcpyDeviceToHost, st));
+        VMT_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int vmt_jump_poly(uint64_t d_lo, uint64_t d_hi, uint64_t* out312) {
+    return guarded([&] {
+        require(out312 != nullptr, VMT_EINVAL, "null argument");
+        const Poly p = Gf2Field::instance().x_pow128(d_lo, d_hi);
+        std::memcpy(out312, p.data(), kPolyWords * 8);
+    });
+}
+
+int vmt_jump_poly_pow2(unsigned q, uint64_t* out312) {
+    return guarded([&] {
+        require(out312 != nullptr, VMT_EINVAL, "null argument");
+        const Poly p = Gf2Field::instance().x_pow2(q);
+        std::memcpy(out312, p.data(), kPolyWords * 8);
+    });
+}
+
+int vmt_charpoly(uint64_t* out313) {
+    return guarded([&] {
+        require(out313 != nullptr, VMT_EINVAL, "null argument");
+        const auto& p = Gf2Field::instance().charpoly();
+        std::memcpy(out313, p.data(), kFullWords * 8);
+    });
+}
+
+int vmt_set_tuning(vmt_handle h, unsigned max_chunks, int variant) {
+    return guarded([&] {
+        require(h != nullptr, VMT_EINVAL, "null handle");
+        (void)pick_variant(h->L, variant); // validates
+        h->max_chunks = max_chunks;
+        h->variant = variant;
+    });
+}
+
+int vmt_set_profiling(vmt_handle h, int enable) {
+    return guarded([&] {
+        require(h != nullptr, VMT_EINVAL, "null handle");
+        DeviceGuard g(h->device);
+        if (enable && !h->ev[0])
+            for (auto& e : h->ev)
+                VMT_CUDA(cudaEventCreate(&e));
+        h->profile = enable != 0;
+        h->ev_valid = false;
+    });
+}
+
+int vmt_last_timings(vmt_handle h, float* jump_ms, float* gen_ms) {
+    return guarded([&] {
+        require(h != nullptr, VMT_EINVAL, "null handle");
+        require(h->profile && h->ev_valid, VMT_ESTATE, "profiling disabled or no fill recorded");
+        DeviceGuard g(h->device);
+        VMT_CUDA(cudaEventSynchronize(h->ev[2]));
+        float a = 0, b = 0;
+        VMT_CUDA(cudaEventElapsedTime(&a, h->ev[0], h->ev[1]));
+        VMT_CUDA(cudaEventElapsedTime(&b, h->ev[1], h->ev[2]));
+        if (jump_ms)
+            *jump_ms = a;
+        if (gen_ms)
+            *gen_ms = b;
+    });
+}
+
+int vmt_stats(vmt_handle h, uint64_t* gen_launches, uint64_t* jump_launches, uint64_t* other_launches,
+              uint64_t* lane_jumps) {
+    return guarded([&] {
+        require(h != nullptr, VMT_EINVAL, "null handle");
+        if (gen_launches)
+            *gen_launches = h->cnt.gen;
+        if (jump_launches)
+            *jump_launches = h->cnt.jump;
+        if (other_launches)
+            *other_launches = h->cnt.other;
+        if (lane_jumps)
+            *lane_jumps = h->cnt.lane_jumps;
+    });
+}
+
+const char* vmt_status_string(int status) {
+    switch (status) {
+    case VMT_OK: return "ok";
+    case VMT_EINVAL: return "invalid argument";
+    case VMT_ESTATE: return "invalid state (cadence / boundary)";
+    case VMT_EIO: return "I/O or format error";
+    case VMT_ECUDA: return "CUDA error";
+    case VMT_ENOMEM: return "out of memory";
+    default: return "unknown status";
+    }
+}
+
+const char* vmt_last_error(void) { return g_last_error.c_str(); }
+
+int vmt_version(void) { return 100; }
+
+} // extern "C"

@@ -1,0 +1,52 @@
+import json
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200)")
+    config.addinivalue_line("markers", "slow: long-running")
+
+
+@pytest.fixture(scope="session")
+def oracle():
+    from oracle import Oracle
+    return Oracle()
+
+
+@pytest.fixture(scope="session")
+def golden():
+    with open(os.path.join(GOLDEN, "golden.json")) as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="session")
+def gnpz():
+    cache = {}
+
+    def load(name):
+        if name not in cache:
+            path = os.path.join(GOLDEN, name)
+            cache[name] = np.load(path) if name.endswith(".npy") else dict(np.load(path))
+        return cache[name]
+    return load
+
+
+@pytest.fixture(scope="session")
+def full_polys(gnpz):
+    """x^(2^q) mod P for q = 19932..19936 (oracle squaring chain, period-checked)."""
+    return gnpz("xpow2_full.npz")
+
+
+def dephase_poly(oracle, q, full_polys=None):
+    if full_polys is not None and f"q{q}" in full_polys:
+        return full_polys[f"q{q}"]
+    return oracle.x_pow2_mod(q)

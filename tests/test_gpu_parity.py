@@ -1,0 +1,245 @@
+"""GPU parity: the sm_100a kernels, called through the C ABI, against the
+reference's golden vectors and the C oracle. Bit-exact everywhere (integer
+and exactly-rounded conversions)."""
+import hashlib
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2309_16682_b200 as V  # noqa: E402
+from conftest import dephase_poly  # noqa: E402
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def dev_u32(n):
+    return torch.empty(n, dtype=torch.uint32, device="cuda")
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need a CUDA device")
+
+
+def test_appendix_a_l16_q16(golden):
+    row = [r for r in golden["appendixA"] if r["lanes"] == 16 and r["seed"] == 5489][0]
+    g = V.VmtEngine(16, 5489, 16)
+    out = dev_u32(row["count"])
+    g.fill_u32(out)
+    torch.cuda.synchronize()
+    v = host(out)
+    assert list(v[:4]) == row["first4"] and int(v[-1]) == row["last"]
+    assert int(np.bitwise_xor.reduce(v)) == row["xor"] == 0x5E141D5B
+
+
+@pytest.mark.parametrize("q", [6, 8, 16])
+@pytest.mark.parametrize("L", [1, 2, 4, 8, 16])
+def test_engine_streams(golden, gnpz, L, q):
+    streams = gnpz("engine_streams.npz")
+    for e in golden["engine"]:
+        if e["lanes"] != L or e["q"] != q:
+            continue
+        g = V.VmtEngine(L, e["seed"], q)
+        out = dev_u32(e["count"])
+        g.fill_u32(out)
+        v = host(out)
+        assert np.array_equal(v[:4096], streams[f"L{L}_q{q}_s{e['seed']}"])
+        assert sha(v) == e["sha"]
+
+
+def test_query_modes_identical():
+    # test_engine.cpp:81-109 / acceptance.cpp:109-135 (n = 100000)
+    n = 100000
+    a = V.VmtEngine(4, 5489, 8)
+    b = V.VmtEngine(4, 5489, 8)
+    c = V.VmtEngine(4, 5489, 8)
+    d = V.VmtEngine(4, 5489, 8)
+    va = np.array([a.next_u32() for _ in range(n)], np.uint32)
+    vb = np.concatenate([b.next_block16() for _ in range((n + 15) // 16)])[:n]
+    vc = np.concatenate([c.next_block_state() for _ in range(-(-n // 2496))])[:n]
+    vd = np.empty(n, np.uint32)
+    pos = 0
+    for k in (1, 15, 16, 2496, 3, 7777, 10):  # ragged bulk fills, host destination
+        d.fill_u32(vd[pos:pos + k])
+        pos += k
+    d.fill_u32(vd[pos:])
+    assert np.array_equal(va, vb) and np.array_equal(va, vc) and np.array_equal(va, vd)
+
+
+def test_mid_buffer_block16_and_cadence():
+    mixed = V.VmtEngine(4, 42, 6)
+    plain = V.VmtEngine(4, 42, 6)
+    for prefix in (1, 2, 3):
+        for _ in range(prefix):
+            assert mixed.next_u32() == plain.next_u32()
+        buf = mixed.next_block16()
+        assert list(buf) == [plain.next_u32() for _ in range(16)]
+    g = V.VmtEngine(4, 7, 6)
+    g.next_block_state()
+    g.next_u32()
+    with pytest.raises(V.LogicError):
+        g.next_block_state()
+
+
+def test_interleaved_state_after_three_blocks(gnpz):
+    g = V.VmtEngine(4, 31337, 10)
+    for _ in range(3):
+        g.next_block_state()
+    assert np.array_equal(g.interleaved_state(), gnpz("engine_state_L4_q10_s31337_b3.npy"))
+
+
+def test_dephased_state_export(gnpz):
+    ref = gnpz("ref_jumps.npz")["dephased_L32_q16_s5489"]
+    g = V.VmtEngine(32, 5489, 16)
+    assert np.array_equal(g.interleaved_state().reshape(624, 32).T, ref)
+    ref16 = gnpz("ref_jumps.npz")["dephased_L16_q16_s1"]
+    g = V.VmtEngine(16, 1, 16)
+    assert np.array_equal(g.interleaved_state().reshape(624, 16).T, ref16)
+
+
+def test_config4_windows_q16_via_skip(golden):
+    for w in golden["c4_windows_q16"]:
+        g = V.VmtEngine(32, 5489, 16)
+        g.skip(w["start_word"])
+        out = dev_u32(w["count"])
+        g.fill_u32(out)
+        v = host(out)
+        assert list(v[:8]) == w["head"] and sha(v) == w["sha"]
+
+
+@pytest.mark.parametrize("L", [8, 16, 32])
+def test_full_period_default_jump(oracle, full_polys, L):
+    """Library default de-phasing (q = 19937 - log2 L) vs the oracle's
+    polynomial de-phasing (parity pinned transitively)."""
+    q = 19937 - (L.bit_length() - 1)
+    lanes = oracle.dephased_states(5489, L, full_polys[f"q{q}"])
+    g = V.VmtGenerator(5489, V.VmtConfig(L))
+    assert g.jump_exponent() == q
+    assert np.array_equal(g.interleaved_state().reshape(624, L).T, lanes)
+    n = 1 << 20
+    out = dev_u32(n)
+    g.fill_u32(out)
+    v = host(out)
+    assert np.array_equal(v, oracle.vmt_stream(lanes, 0, n))
+    assert int(v[0]) == 3499211612  # output[0] is the scalar first output for seed 5489
+
+
+@pytest.mark.parametrize("max_chunks", [1, 7, 0])
+def test_chunked_fill_appendix_a_l8(golden, max_chunks):
+    row = [r for r in golden["appendixA"] if r["lanes"] == 8][0]  # 2^28 words
+    g = V.VmtEngine(8, 42, 16)
+    g.set_tuning(max_chunks=max_chunks)
+    out = dev_u32(row["count"])
+    g.fill_u32(out)
+    v = host(out)
+    assert int(np.bitwise_xor.reduce(v)) == row["xor"] == 0x3837517C
+    assert list(v[:4]) == row["first4"] and int(v[-1]) == row["last"]
+
+
+def test_xor_checksum_matches_store(golden):
+    row = [r for r in golden["appendixA"] if r["lanes"] == 16 and r["seed"] == 5489][0]
+    g = V.VmtEngine(16, 5489, 16)
+    assert g.checksum_xor(row["count"]) == row["xor"]
+    # continuation: xor of the next window equals the stored next window
+    a = V.VmtEngine(16, 5489, 16)
+    a.skip(row["count"])
+    out = dev_u32(12345)
+    a.fill_u32(out)
+    assert g.checksum_xor(12345) == int(np.bitwise_xor.reduce(host(out)))
+
+
+@pytest.mark.parametrize("L", [8, 16, 32])
+def test_ragged_positions(oracle, L):
+    q = 8
+    lanes = oracle.dephased_states(99, L, oracle.x_pow2_mod(q))
+    total = 3 * 624 * L + 1001
+    ref = oracle.vmt_stream(lanes, 0, total)
+    g = V.VmtEngine(L, 99, q)
+    got = []
+    for k in (0, 1, 2, 3, 5, 624 * L - 11, 4, 624 * L + 1, 7, 1000):
+        t = dev_u32(max(k, 1))
+        g.fill_u32(t, k)
+        got.append(host(t)[:k])
+    rest = total - sum(len(x) for x in got)
+    t = dev_u32(rest)
+    g.fill_u32(t)
+    got.append(host(t))
+    assert np.array_equal(np.concatenate(got), ref)
+
+
+def test_float_conversions(oracle):
+    L, q, n = 8, 16, (1 << 20) + 6
+    lanes = oracle.dephased_states(42, L, oracle.x_pow2_mod(q))
+    u = oracle.vmt_stream(lanes, 0, 2 * n)
+    f32 = ((u[:n] >> 8).astype(np.float32) * np.float32(2.0 ** -24))
+    f64 = u[:n].astype(np.float64) * 2.0 ** -32
+    r3 = (u[:n].astype(np.float64) + 0.5) * 2.0 ** -32
+    a, b = u[0:2 * n:2], u[1:2 * n:2]
+    r53 = ((a >> 5).astype(np.float64) * 67108864.0 + (b >> 6).astype(np.float64)) * 2.0 ** -53
+    g = V.VmtEngine(L, 42, q)
+    t = torch.empty(n, dtype=torch.float32, device="cuda")
+    g.fill_f32(t)
+    assert np.array_equal(host(t).view(np.uint32), f32.view(np.uint32))
+    assert host(t).max() < 1.0
+    for rule, ref in ((V.VMT_F64_32, f64), (V.VMT_F64_REAL3, r3), (V.VMT_F64_RES53, r53)):
+        g = V.VmtEngine(L, 42, q)
+        t = torch.empty(n, dtype=torch.float64, device="cuda")
+        g.fill_f64(t, rule=rule)
+        assert np.array_equal(host(t).view(np.uint64), ref.view(np.uint64)), rule
+
+
+def test_batch_generators(golden, oracle):
+    rows = {r["seed"]: r for r in golden["appendixA"] if r["lanes"] == 16 and r["count"] == 1 << 20}
+    n, ngen = 1 << 20, 1024
+    out = dev_u32(n * ngen)
+    V.batch_fill_u32(out, 1, ngen, 16, n, jump_exponent=16)
+    v = host(out).reshape(ngen, n)
+    assert int(np.bitwise_xor.reduce(v[0])) == rows[1]["xor"] == 0xA63A3C52
+    assert int(np.bitwise_xor.reduce(v[1023])) == rows[1024]["xor"] == 0xD18F46A1
+    poly = oracle.x_pow2_mod(16)
+    for gi in (5, 511, 777):
+        lanes = oracle.dephased_states(gi + 1, 16, poly)
+        assert np.array_equal(v[gi, :20000], oracle.vmt_stream(lanes, 0, 20000))
+
+
+def test_jump_states_config5(gnpz, oracle):
+    c5 = gnpz("c5_ref.npz")
+    seeds = np.arange(1, 4097, dtype=np.uint32)
+    st = V.seed_states(seeds)
+    assert np.array_equal(st[0], oracle.seed_words(1))
+    d = oracle.mt64(7, 4096)
+    out = V.jump_states(st, d)
+    for i in range(8):
+        assert np.array_equal(oracle.mt_stream_from_words(out[i], 624), c5[f"s{i + 1}"]), i
+    for i in (100, 2047, 4095):
+        j = oracle.poly_jump(st[i], oracle.x_pow_mod(int(d[i])))
+        assert np.array_equal(out[i], j)
+
+
+def test_create_from_states_roundtrip(oracle):
+    lanes = oracle.dephased_states(7, 8, oracle.x_pow2_mod(12))
+    g = V.VmtGenerator(0, lane_states=lanes)
+    out = dev_u32(50000)
+    g.fill_u32(out)
+    assert np.array_equal(host(out), oracle.vmt_stream(lanes, 0, 50000))
+
+
+def test_empty_fill_and_host_destination():
+    g = V.VmtEngine(16, 5489, 16)
+    g.fill_u32(dev_u32(1), 0)
+    h = np.empty(10000, np.uint32)
+    g.fill_u32(h)
+    r = V.VmtEngine(16, 5489, 16)
+    d = dev_u32(10000)
+    r.fill_u32(d)
+    assert np.array_equal(h, host(d))
