@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""VMT19937 on B200 -- benchmark for the driver contract.
+
+Workload (BASELINE.json configs[3], the one the metric is quoted on: "uint32
+random numbers/sec per GPU and whole box (1/2/4/8 B200)"): one VMT19937 stream
+with L = 32 lanes, seed 5489 (init_genrand), lanes de-phased by the library
+default jump-ahead (q = 19937 - log2 32 = 19932), 2^34 uint32 words (64 GiB)
+per step, partitioned into contiguous ranges across the N ranks (strong
+scaling; each rank jumps to its range, no data-path collective). A step is one
+pass over the whole 2^34-word range; consecutive steps generate consecutive
+2^34-word ranges of the stream (so every step pays the chunk-positioning jump
+work, nothing is cached between steps). Output goes to a preallocated HBM
+buffer of the rank's share (64 GiB at N=1 -- larger than L2, no flush needed).
+
+value    : whole-job uint32/s over all ranks, CUDA events on the launching
+           stream, max over ranks (positioning jumps + generation kernels).
+e2e      : the same workload through the public API into pinned HOST memory
+           (device->host copy of every word inside the timed region).
+roofline : the generation kernel (vmt_gen_kernel) alone: algorithmic bytes
+           (4 B per output word written, 0 B read) / its CUDA-event duration,
+           against MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline : the unmodified reference library (oracle/_ref) on the host
+           cores, one VmtEngine<16> per core writing next_block_state into its
+           slice of a DRAM buffer (L=32 is not supported by the reference).
+
+--impl reference times that reference CPU path alone on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+TOTAL_WORDS = 1 << 34
+LANES = 32
+SEED = 5489
+METRIC = "uint32 random numbers/sec per GPU and whole box (1/2/4/8 B200); % of HBM write BW"
+UNIT = "uint32/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--words", type=int, default=TOTAL_WORDS)
+    ap.add_argument("--mode", choices=["store", "xor"], default="store")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--chunks", type=int, default=0)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- clocks --
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) < 8:
+                continue
+            for i, nm in enumerate(names):
+                if r[4 + i].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md, 6.65 TB/s)"
+
+
+def profiled_traffic():
+    """dram read+write bytes per gen-kernel launch from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "gen_kernel_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------ CPU baseline --
+def reference_cpu(words: int, threads: int, q: int = 16):
+    """The unmodified reference library on the host: `threads` independent
+    VmtEngine<16> each writing next_block_state into its own slice (BASELINE.md
+    section 3). Returns (words/s, seconds, checksum)."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import RefLib
+    ref = RefLib()
+    bw = 624 * 16
+    per = -(-words // threads)
+    per = -(-per // bw) * bw
+    buf = np.empty(per * threads, np.uint32)
+    buf[::1024] = 0  # touch pages outside the timed region
+    ref.lib.vref_prepare_ladder(q)
+    secs, x = ref.bench_threads(16, SEED, q, per, threads, buf)
+    return per * threads / secs, secs, x, per * threads
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    words = args.words
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, s, x, done = reference_cpu(words, threads)
+        if i >= args.warmup:
+            vals.append((v, s))
+    value = statistics.median(v for v, _ in vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": statistics.median(s for _, s in vals) * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded generator)",
+        "config": {"workload": "c4: L=32 VMT19937 stream, 2^34 uint32 per step", "total_words": words,
+                   "reference_lanes": 16, "reference_jump_exponent": 16,
+                   "note": "reference engine supports L<=16 (engine.hpp:43); M=16 AVX-512 engines, q=16 "
+                           "(throughput is independent of q; full-period matrices take ~50 h)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{words} uint32 per step, {threads} threads x VmtEngine<16>::next_block_state "
+                                   f"into DRAM ({cpu_model()})"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# -------------------------------------------------------------------- ours --
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2309_16682_b200 as V
+    from paper_2309_16682_b200.dist import combine_xor, max_over_ranks, partition
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    T = args.words
+    start, count = partition(T, world, rank)
+
+    g = V.VmtGenerator(SEED, V.VmtConfig(LANES), device=local)
+    g.set_tuning(max_chunks=args.chunks, variant=args.variant)
+    out = torch.empty(count, dtype=torch.uint32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        if args.mode == "store":
+            g.fill_u32(out)
+        else:
+            g.checksum_xor(count, stream=stream.cuda_stream or 1)
+        g.skip(T - count)  # the other ranks' share of this step
+
+    g.seek(start)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    s0 = g.stats()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    e1.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop()
+    s1 = g.stats()
+    ms = e0.elapsed_time(e1) / args.steps
+    ms = max_over_ranks(ms, dev)
+    launches = sum(s1[k] - s0[k] for k in ("gen_launches", "jump_launches", "other_launches"))
+
+    # -- generation kernel alone (CUDA events around it on the same stream)
+    g.set_profiling(True)
+    jumps, gens = [], []
+    for _ in range(args.steps):
+        step()
+        j, gm = g.last_timings()
+        jumps.append(j)
+        gens.append(gm)
+    g.set_profiling(False)
+    gen_ms = max_over_ranks(statistics.mean(gens), dev)
+    jump_ms = max_over_ranks(statistics.mean(jumps), dev)
+
+    # -- global checksum of one full 2^34 range (config 4 verification)
+    g.seek(start)
+    csum = combine_xor(g.checksum_xor(count), dev)
+    torch.cuda.synchronize(dev)
+
+    # -- end to end into pinned host memory through the public API
+    e2e = None
+    if not args.no_e2e and args.mode == "store":
+        del out
+        torch.cuda.empty_cache()
+        try:
+            host = torch.empty(count, dtype=torch.uint32, pin_memory=True)
+            kind = "pinned"
+        except Exception:
+            host = np.empty(count, np.uint32)
+            kind = "pageable"
+        g.seek(start)
+        g.fill_u32(host)  # warm-up
+        g.skip(T - count)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            g.fill_u32(host)
+            g.skip(T - count)
+        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+        e2e_s = max_over_ranks(e2e_s, dev)
+        e2e = {"value": T / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": T * 4,
+               "ms_per_step": e2e_s * 1e3, "host_buffer": kind, "steps": args.e2e_steps}
+        del host
+
+    peak, peak_src = measured_peak()
+    bytes_per_launch = count * 4
+    achieved = bytes_per_launch / (gen_ms * 1e-3) / 1e9
+    traffic = profiled_traffic()
+    line = {
+        "metric": METRIC, "value": T / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded generator, no inputs)",
+        "config": {"workload": "c4: one L=32 VMT19937 stream, seed 5489, default full-period de-phasing "
+                               "(q=19932), 2^34 uint32 per step partitioned across ranks",
+                   "total_words": T, "lanes": LANES, "jump_exponent": g.jump_exponent(), "mode": args.mode,
+                   "per_rank_words": count, "l2": "output 64 GiB/N per step >> 126 MB L2 (no flush needed)",
+                   "parallelism": f"stream partition x{world}"},
+        "gpu_launches": launches,
+        "per_gpu_value": count / (ms * 1e-3),
+        "gen_kernel_ms": gen_ms, "positioning_jump_ms": jump_ms,
+        "gen_only_value": T / (max(gen_ms, 1e-9) * 1e-3) if world == 1 else None,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+                     "kernel": "vmt_gen_kernel", "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": bytes_per_launch},
+        "checksum_xor": f"0x{csum:08x}",
+        "clocks": clk,
+        "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            v, s, x, done = reference_cpu(1 << 32, threads)
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+                                    "sample": f"{done} uint32 (2^32), {threads} threads x VmtEngine<16> "
+                                              f"next_block_state into DRAM, q=16 ({cpu_model()}); "
+                                              "L=32 unsupported by the reference"}
+        except Exception as e:  # the reference build is optional on the box
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                                    "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -97,6 +97,8 @@ int vmt_synchronize(vmt_handle h);
 
 /* Advances the position by d words (new; arbitrary 64-bit distance). */
 int vmt_skip(vmt_handle h, uint64_t d);
+/* Sets the absolute stream position (forward or backward; new). */
+int vmt_seek(vmt_handle h, uint64_t pos);
 
 /* VmtEngine::interleaved_state (engine.hpp:100): 624*lanes words, state of
  * the most recently regenerated block (the de-phased seed states before the

@@ -236,6 +236,9 @@ class VmtGenerator:
     def skip(self, d: int) -> None:
         check(lib.vmt_skip(self._h, d))
 
+    def seek(self, pos: int) -> None:
+        check(lib.vmt_seek(self._h, pos))
+
     def set_tuning(self, max_chunks: int = 0, variant: int = 0) -> None:
         check(lib.vmt_set_tuning(self._h, max_chunks, variant))
 

@@ -21,7 +21,7 @@ EXPORTS = [
     "vmt_full_period_exponent", "vmt_create", "vmt_create_from_states", "vmt_destroy", "vmt_lanes",
     "vmt_state_words", "vmt_jump_exponent", "vmt_position", "vmt_next_u32", "vmt_next_block16",
     "vmt_next_block_state", "vmt_fill_u32", "vmt_fill_f32", "vmt_fill_f64", "vmt_checksum_xor",
-    "vmt_skip", "vmt_synchronize", "vmt_export_state", "vmt_batch_fill_u32", "vmt_jump_states", "vmt_seed_states",
+    "vmt_skip", "vmt_seek", "vmt_synchronize", "vmt_export_state", "vmt_batch_fill_u32", "vmt_jump_states", "vmt_seed_states",
     "vmt_jump_poly", "vmt_jump_poly_pow2", "vmt_charpoly", "vmt_set_tuning", "vmt_set_profiling", "vmt_last_timings", "vmt_stats",
     "vmt_status_string", "vmt_last_error", "vmt_version",
 ]
@@ -67,6 +67,7 @@ def _load() -> ctypes.CDLL:
         "vmt_fill_f64": (c.c_int, [H, c.c_void_p, c.c_uint64, c.c_int, c.c_void_p]),
         "vmt_checksum_xor": (c.c_int, [H, c.c_uint64, u32p, c.c_void_p]),
         "vmt_skip": (c.c_int, [H, c.c_uint64]),
+        "vmt_seek": (c.c_int, [H, c.c_uint64]),
         "vmt_synchronize": (c.c_int, [H]),
         "vmt_export_state": (c.c_int, [H, c.c_void_p]),
         "vmt_batch_fill_u32": (c.c_int, [c.c_uint32, c.c_uint, c.c_uint, c.c_uint, c.c_uint64, c.c_void_p,

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -69,6 +70,10 @@ int guarded(F&& f) {
     }
 }
 
+// Host-destination fills are staged through device memory in segments of
+// this many stream words (two segments in flight).
+constexpr std::uint64_t kHostSegmentWords = 1ull << 28;
+
 bool valid_lanes(unsigned L) { return L == 1 || L == 2 || L == 4 || L == 8 || L == 16 || L == 32; }
 
 unsigned log2u(unsigned L) {
@@ -82,76 +87,56 @@ unsigned log2u(unsigned L) {
 using GenFn = void (*)(GenParams);
 
 struct Variant {
-    int L = 0, R = 0, NT = 0, SMEM = 0;
+    int id = 0, L = 0, R = 0, VW = 0, NT = 0, SMEM = 0;
     GenFn fn[6][2] = {};
 };
 
-template <int L, int R, int MODE>
+template <int L, int R, int VW, int MODE>
 void fill_mode(Variant& v) {
-    v.fn[MODE][0] = vmt_gen_kernel<L, R, MODE, false>;
-    v.fn[MODE][1] = vmt_gen_kernel<L, R, MODE, true>;
+    v.fn[MODE][0] = vmt_gen_kernel<L, R, VW, MODE, false>;
+    v.fn[MODE][1] = vmt_gen_kernel<L, R, VW, MODE, true>;
 }
 
-template <int L, int R>
-Variant make_variant() {
+template <int L, int R, int VW>
+Variant make_variant(int id) {
     Variant v;
+    v.id = id;
     v.L = L;
     v.R = R;
-    v.NT = GenShape<L, R>::NT;
-    v.SMEM = GenShape<L, R>::SMEM;
-    fill_mode<L, R, MODE_U32>(v);
-    fill_mode<L, R, MODE_XOR>(v);
-    fill_mode<L, R, MODE_F32>(v);
-    fill_mode<L, R, MODE_F64>(v);
-    fill_mode<L, R, MODE_F64_REAL3>(v);
-    fill_mode<L, R, MODE_F64_RES53>(v);
+    v.VW = VW;
+    v.NT = GenShape<L, R, VW>::NT;
+    v.SMEM = GenShape<L, R, VW>::SMEM;
+    fill_mode<L, R, VW, MODE_U32>(v);
+    fill_mode<L, R, VW, MODE_XOR>(v);
+    fill_mode<L, R, VW, MODE_F32>(v);
+    fill_mode<L, R, VW, MODE_F64>(v);
+    fill_mode<L, R, VW, MODE_F64_REAL3>(v);
+    fill_mode<L, R, VW, MODE_F64_RES53>(v);
     return v;
 }
 
-// variant ids: 0 auto; 1 R=13; 2 R=4; 3 R=2; 4 R=8; 5 R=1 (run length R =
-// consecutive words per thread per window; see GenShape)
-int run_length_of(int variant) {
-    switch (variant) {
-    case 1: return 13;
-    case 2: return 4;
-    case 3: return 2;
-    case 4: return 8;
-    case 5: return 1;
-    default: return -1;
-    }
-}
-
+// Kernel shape variants (vmt_set_tuning): run length R = consecutive words
+// per thread per window, VW = lanes per thread. The first entry per lane
+// count is the default.
+//   id 1: R=13 VW=4   id 2: R=4 VW=4   id 3: R=13 VW=2   id 4: R=13 VW=1
+//   id 5: R=1 VW=4
 const Variant& pick_variant(unsigned L, int variant) {
-    static const Variant v32[] = {make_variant<32, 13>(), make_variant<32, 4>(), make_variant<32, 2>(),
-                                  make_variant<32, 8>()};
-    static const Variant v16[] = {make_variant<16, 13>(), make_variant<16, 4>(), make_variant<16, 2>(),
-                                  make_variant<16, 1>()};
-    static const Variant v8[] = {make_variant<8, 13>(), make_variant<8, 4>(), make_variant<8, 2>(),
-                                 make_variant<8, 1>()};
-    static const Variant v4[] = {make_variant<4, 4>(), make_variant<4, 1>()};
-    static const Variant v2 = make_variant<2, 1>(), v1 = make_variant<1, 1>();
-    auto find = [&](const Variant* vs, int n, int R) -> const Variant& {
-        for (int i = 0; i < n; ++i)
-            if (vs[i].R == R)
-                return vs[i];
-        throw VmtError(VMT_EINVAL, "unknown kernel variant for this lane count");
+    static const std::vector<Variant> table = {
+        make_variant<32, 13, 4>(1), make_variant<32, 4, 4>(2), make_variant<32, 13, 2>(3),
+        make_variant<32, 13, 1>(4),
+        make_variant<16, 13, 4>(1), make_variant<16, 13, 2>(3), make_variant<16, 13, 1>(4),
+        make_variant<16, 1, 4>(5),
+        make_variant<8, 13, 4>(1), make_variant<8, 13, 2>(3), make_variant<8, 13, 1>(4), make_variant<8, 1, 4>(5),
+        make_variant<4, 13, 1>(4), make_variant<4, 1, 4>(5), make_variant<4, 13, 2>(3),
+        make_variant<2, 13, 1>(4), make_variant<2, 1, 2>(5),
+        make_variant<1, 1, 1>(5),
     };
-    const int R = run_length_of(variant);
-    switch (L) {
-    case 32: return find(v32, 4, variant == 0 ? 2 : R);
-    case 16: return find(v16, 4, variant == 0 ? 1 : R);
-    case 8: return find(v8, 4, variant == 0 ? 1 : R);
-    case 4: return find(v4, 2, variant == 0 ? 1 : R);
-    case 2:
-        if (variant != 0 && R != 1)
-            throw VmtError(VMT_EINVAL, "unknown kernel variant for this lane count");
-        return v2;
-    case 1:
-        if (variant != 0 && R != 1)
-            throw VmtError(VMT_EINVAL, "unknown kernel variant for this lane count");
-        return v1;
-    default: throw VmtError(VMT_EINVAL, "lanes must be one of 1, 2, 4, 8, 16, 32");
-    }
+    for (const Variant& v : table)
+        if (v.L == (int)L && (variant == 0 || v.id == variant))
+            return v;
+    if (!valid_lanes(L))
+        throw VmtError(VMT_EINVAL, "lanes must be one of 1, 2, 4, 8, 16, 32");
+    throw VmtError(VMT_EINVAL, "unknown kernel variant for this lane count");
 }
 
 struct DeviceInfo {
@@ -424,6 +409,9 @@ struct vmt_generator {
     std::uint32_t* hsmall = nullptr; // pinned 4-byte readback
 
     std::map<std::uint64_t, std::unique_ptr<PolySet>> polycache; // blocks-per-chunk -> J^c
+    std::map<std::uint64_t, std::unique_ptr<DevBuf<std::uint64_t>>> skipcache; // block delta -> x^(624 delta)
+    cudaStream_t copy_stream = nullptr;                                  // D2H of host fills
+    cudaEvent_t seg_gen[2] = {nullptr, nullptr}, seg_copy[2] = {nullptr, nullptr};
     unsigned max_chunks = 0;
     int variant = 0;
     Counters cnt;
@@ -514,11 +502,23 @@ void reposition(vmt_generator* h, std::uint64_t target, cudaStream_t st) {
         from = h->base.p;
         delta = target;
     }
-    Gf2Field& F = Gf2Field::instance();
-    // 624*delta may exceed 64 bits for huge skips
-    const unsigned __int128 d = (unsigned __int128)624u * delta;
-    std::vector<Poly> polys{F.x_pow128((std::uint64_t)d, (std::uint64_t)(d >> 64))};
-    const std::uint64_t* dp = upload_polys(h, polys, st);
+    // x^(624*delta) mod P, cached per distance (repeated strides are common:
+    // a rank skipping the other ranks' shares, or seeking back to a range)
+    auto it = h->skipcache.find(delta);
+    if (it == h->skipcache.end()) {
+        if (h->skipcache.size() >= 16)
+            h->skipcache.clear();
+        Gf2Field& F = Gf2Field::instance();
+        // 624*delta may exceed 64 bits for huge skips
+        const unsigned __int128 d = (unsigned __int128)624u * delta;
+        const Poly poly = F.x_pow128((std::uint64_t)d, (std::uint64_t)(d >> 64));
+        auto& slot = h->skipcache[delta];
+        slot.reset(new DevBuf<std::uint64_t>());
+        slot->reserve(kPolyWords);
+        VMT_CUDA(cudaMemcpy(slot->p, poly.data(), kPolyWords * 8, cudaMemcpyHostToDevice));
+        it = h->skipcache.find(delta);
+    }
+    const std::uint64_t* dp = it->second->p;
     AffineJobs a;
     a.n = (int)h->L;
     a.div = (int)h->L;
@@ -547,7 +547,7 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     const int esz = (mode == MODE_U32 || mode == MODE_F32 || mode == MODE_XOR) ? 4 : 8;
     bool vec = false;
     if (mode != MODE_XOR && mode != MODE_F64_RES53) {
-        const int V = v.L >= 4 ? 4 : v.L;
+        const int V = v.L >= v.VW ? v.VW : v.L;
         const std::uintptr_t a = reinterpret_cast<std::uintptr_t>(out);
         const std::uint64_t e = (std::uint64_t)(a / (std::uintptr_t)esz);
         const int need = (esz == 8) ? 2 : V; // double2 / VecT<V> stores
@@ -562,6 +562,10 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     if (h->max_chunks)
         C = std::min<std::uint64_t>(C, h->max_chunks);
     C = std::min<std::uint64_t>(C, nb);
+    static const bool debug = std::getenv("VMT_DEBUG") != nullptr;
+    if (debug)
+        std::fprintf(stderr, "[vmt] L=%u R=%d NT=%d smem=%d occ=%d chunks=%llu blocks=%llu mode=%d vec=%d\n", h->L,
+                     v.R, v.NT, v.SMEM, occ, (unsigned long long)C, (unsigned long long)nb, mode, (int)vec);
     const std::uint64_t B = (nb + C - 1) / C;
     C = (nb + B - 1) / B;
 
@@ -653,11 +657,36 @@ void fill_generic(vmt_generator* h, void* dst, std::uint64_t n, int mode, void* 
     if (dev) {
         gpu_generate(h, mode, dst, words, st, nullptr);
     } else {
-        const std::uint64_t bytes = n * (std::uint64_t)esz;
-        h->scratch.reserve((bytes + 3) / 4 + 4);
-        gpu_generate(h, mode, h->scratch.p, words, st, nullptr);
-        VMT_CUDA(cudaMemcpyAsync(dst, h->scratch.p, bytes, cudaMemcpyDeviceToHost, st));
-        VMT_CUDA(cudaStreamSynchronize(st));
+        // host destination: generate in segments into two device staging
+        // buffers and copy each one out on a second stream while the next
+        // segment is generated (pinned destinations overlap fully)
+        const std::uint64_t per_elem_words = (mode == MODE_F64_RES53) ? 2 : 1;
+        const std::uint64_t seg_elems = std::min<std::uint64_t>(n, kHostSegmentWords / per_elem_words);
+        const std::uint64_t seg_words_cap = seg_elems * (std::uint64_t)esz / 4; // scratch words per half
+        h->scratch.reserve(2 * seg_words_cap + 8);
+        if (!h->copy_stream) {
+            VMT_CUDA(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+            for (int i = 0; i < 2; ++i) {
+                VMT_CUDA(cudaEventCreateWithFlags(&h->seg_gen[i], cudaEventDisableTiming));
+                VMT_CUDA(cudaEventCreateWithFlags(&h->seg_copy[i], cudaEventDisableTiming));
+            }
+        }
+        std::uint64_t done = 0;
+        for (int i = 0; done < n; ++i) {
+            const int half = i & 1;
+            const std::uint64_t ne = std::min<std::uint64_t>(seg_elems, n - done);
+            std::uint32_t* buf = h->scratch.p + half * seg_words_cap;
+            if (i >= 2)
+                VMT_CUDA(cudaStreamWaitEvent(st, h->seg_copy[half], 0));
+            gpu_generate(h, mode, buf, ne * per_elem_words, st, nullptr);
+            VMT_CUDA(cudaEventRecord(h->seg_gen[half], st));
+            VMT_CUDA(cudaStreamWaitEvent(h->copy_stream, h->seg_gen[half], 0));
+            VMT_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + done * esz, buf, ne * esz, cudaMemcpyDeviceToHost,
+                                     h->copy_stream));
+            VMT_CUDA(cudaEventRecord(h->seg_copy[half], h->copy_stream));
+            done += ne;
+        }
+        VMT_CUDA(cudaStreamSynchronize(h->copy_stream));
     }
     h->pos = h->gpos;
     h->mark(st);
@@ -789,6 +818,14 @@ int vmt_destroy(vmt_handle h) {
             for (auto& e : h->ev)
                 if (e)
                     cudaEventDestroy(e);
+            if (h->copy_stream) {
+                cudaStreamSynchronize(h->copy_stream);
+                cudaStreamDestroy(h->copy_stream);
+                for (int i = 0; i < 2; ++i) {
+                    cudaEventDestroy(h->seg_gen[i]);
+                    cudaEventDestroy(h->seg_copy[i]);
+                }
+            }
             cudaStreamDestroy(h->own);
             delete h;
         }
@@ -898,6 +935,21 @@ int vmt_synchronize(vmt_handle h) {
     });
 }
 
+int vmt_seek(vmt_handle h, uint64_t pos) {
+    return guarded([&] {
+        require(h != nullptr, VMT_EINVAL, "null handle");
+        if (pos >= h->pos && pos <= h->gpos) {
+            h->pos = pos; // forward inside the words already staged on the host
+            return;
+        }
+        // drop staging; the GPU state is re-positioned lazily by the next
+        // fill (forward from the current block, or from block 0 backwards)
+        h->pos = pos;
+        h->gpos = pos;
+        h->hstage_start = pos;
+    });
+}
+
 int vmt_skip(vmt_handle h, uint64_t d) {
     return guarded([&] {
         require(h != nullptr, VMT_EINVAL, "null handle");
@@ -968,7 +1020,7 @@ int vmt_batch_fill_u32(uint32_t seed0, unsigned ngen, unsigned lanes, unsigned j
             out = scratch.p;
         }
         const bool vec = (reinterpret_cast<std::uintptr_t>(out) % 16 == 0) && (n_per_gen % 4 == 0);
-        GenFn fn = v.fn[MODE_U32][vec && v.L >= 4 ? 1 : 0];
+        GenFn fn = v.fn[MODE_U32][vec ? 1 : 0];
         prepare_gen(device, fn, v.NT, v.SMEM);
         GenParams p{};
         p.chunk_states = states.p;

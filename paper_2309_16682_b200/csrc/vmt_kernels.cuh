@@ -126,14 +126,20 @@ struct VecT<1> {
 
 // CTA shape: a CTA owns all L lanes of one chunk; thread (rho, q) computes
 // R consecutive sequence words of lanes q*V .. q*V+V-1 in every window.
-template <int L, int R>
+// VW (1, 2 or 4) is the vector width: smaller VW = more threads per lane
+// state (more warps per SM for the same shared memory).
+template <int L, int R, int VW = 4>
 struct GenShape {
-    static constexpr int V = L >= 4 ? 4 : L;      // lanes per thread (vector width)
+    static constexpr int V = L >= VW ? VW : L;    // lanes per thread (vector width)
     static constexpr int Q = L / V;               // threads across a slot row
     static constexpr int RUNS = kWin / R;         // runs per window
     static constexpr int NT = RUNS * Q;           // threads per CTA
     static constexpr int SLOTS = kRing + R;       // ring + mirror of slots [0, R)
     static constexpr int SMEM = SLOTS * L * 4;
+    // CTAs per SM that shared memory allows (227 KB usable, 1 KB reserved per CTA)
+    static constexpr int SMEM_CTAS = (227 * 1024) / (SMEM + 1024) > 0 ? (227 * 1024) / (SMEM + 1024) : 1;
+    // registers are capped so that they never limit occupancy below that
+    static constexpr int MINB = (SMEM_CTAS * NT > 2048) ? (2048 / NT > 0 ? 2048 / NT : 1) : SMEM_CTAS;
     static_assert(kWin % R == 0 && kN % R == 0 && kRing % R == 0, "run length must divide 208");
 };
 
@@ -231,11 +237,11 @@ __device__ __forceinline__ void emit(const std::uint32_t* w, unsigned long long 
 // the run's first p; a: slot of x_{p+397}; wsl: slot receiving x_{p+624}.
 // All ring loads are issued before any ring store (the stores go to slots no
 // thread reads in this window), so the compiler is free to overlap them.
-template <int L, int R, int MODE, bool VEC, bool FULL>
+template <int L, int R, int VW, int MODE, bool VEC, bool FULL>
 __device__ __forceinline__ void gen_window(std::uint32_t* ring, int base, int a, int wsl, int q,
                                            unsigned long long g0, const GenParams& p, void* out,
                                            std::uint32_t* acc) {
-    constexpr int V = GenShape<L, R>::V;
+    constexpr int V = GenShape<L, R, VW>::V;
     using VT = typename VecT<V>::T;
     using E = typename ElemT<MODE>::T;
     std::uint32_t X[R + 1][V], M[R][V];
@@ -298,9 +304,9 @@ __device__ __forceinline__ void save_boundary(const std::uint32_t* ring, int blk
 
 // One CTA = one chunk (all L lanes). Dynamic shared memory GenShape::SMEM
 // bytes: ring[slot][L].
-template <int L, int R, int MODE, bool VEC>
-__global__ void __launch_bounds__(GenShape<L, R>::NT) vmt_gen_kernel(GenParams p) {
-    using S = GenShape<L, R>;
+template <int L, int R, int VW, int MODE, bool VEC>
+__global__ void __launch_bounds__(GenShape<L, R, VW>::NT, GenShape<L, R, VW>::MINB) vmt_gen_kernel(GenParams p) {
+    using S = GenShape<L, R, VW>;
     constexpr int V = S::V;
     using VT = typename VecT<V>::T;
     extern __shared__ __align__(16) std::uint32_t ring[];
@@ -344,7 +350,7 @@ __global__ void __launch_bounds__(GenShape<L, R>::NT) vmt_gen_kernel(GenParams p
     for (unsigned long long blk = b_lo; blk < b_hi; ++blk) {
         if (save_here && blk == p.save_block)
             save_boundary<L>(ring, blk_base_slot, p.save_state, tid, S::NT);
-        const bool full = batch || (blk * bw >= p.pos_begin && (blk + 1) * bw <= p.pos_end);
+        const bool full = blk * bw >= p.pos_begin && (blk + 1) * bw <= p.pos_end;
 #pragma unroll 1
         for (int third = 0; third < 3; ++third) {
             int wstart = blk_base_slot + third * kWin;
@@ -359,9 +365,9 @@ __global__ void __launch_bounds__(GenShape<L, R>::NT) vmt_gen_kernel(GenParams p
                 wsl -= kRing;
             const unsigned long long g0 = blk * bw + (unsigned long long)(third * kWin + rho * R) * L + q * V;
             if (full)
-                gen_window<L, R, MODE, VEC, true>(ring, base, a, wsl, q, g0, p, out, acc);
+                gen_window<L, R, VW, MODE, VEC, true>(ring, base, a, wsl, q, g0, p, out, acc);
             else
-                gen_window<L, R, MODE, VEC, false>(ring, base, a, wsl, q, g0, p, out, acc);
+                gen_window<L, R, VW, MODE, VEC, false>(ring, base, a, wsl, q, g0, p, out, acc);
             __syncthreads();
         }
         blk_base_slot += kN;
@@ -408,7 +414,7 @@ struct JumpParams {
     int p_a, p_b, p_c;
 };
 
-constexpr int kJumpWarps = 8;
+constexpr int kJumpWarps = 1;
 constexpr int kSeqRing = 1024;
 constexpr int kGroups = 998; // 998 * 20 = 19960 >= 19937 coefficient steps
 
@@ -436,11 +442,10 @@ __device__ __forceinline__ void jump_pair(std::uint32_t (&Y)[20], const std::uin
 }
 
 __device__ __forceinline__ unsigned poly_bits20(const std::uint32_t* p32, int i) {
+    // 20 coefficient bits starting at bit i (p32 in shared memory)
     const int w = i >> 5, o = i & 31;
-    unsigned v = __ldg(p32 + w) >> o;
-    if (o > 12)
-        v |= __ldg(p32 + w + 1) << (32 - o);
-    return v & 0xFFFFFu;
+    const unsigned long long two = ((unsigned long long)p32[w + 1] << 32) | p32[w];
+    return (unsigned)(two >> o) & 0xFFFFFu;
 }
 
 __device__ __forceinline__ void jump_produce(std::uint32_t* seq, int m) {
@@ -460,13 +465,17 @@ __device__ __forceinline__ void jump_load20(const std::uint32_t* seq, int start,
     }
 }
 
-__global__ void __launch_bounds__(kJumpWarps * 32) vmt_jump_kernel(JumpParams p) {
-    __shared__ __align__(16) std::uint32_t seq_all[kJumpWarps][kSeqRing];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int job = blockIdx.x * kJumpWarps + warp;
+// One warp per CTA, so everything derived from the job index (the polynomial
+// coefficients driving the branches) is CTA-uniform.
+#ifndef VMT_JUMP_MINB
+#define VMT_JUMP_MINB 32
+#endif
+__global__ void __launch_bounds__(32, VMT_JUMP_MINB) vmt_jump_kernel(JumpParams p) {
+    __shared__ __align__(16) std::uint32_t seq[kSeqRing];
+    const int lane = threadIdx.x;
+    const int job = blockIdx.x;
     if (job >= p.njobs)
         return;
-    std::uint32_t* seq = seq_all[warp];
     long long so, dof;
     int pidx;
     if (p.job_src != nullptr) {
@@ -489,7 +498,16 @@ __global__ void __launch_bounds__(kJumpWarps * 32) vmt_jump_kernel(JumpParams p)
         jump_produce(seq, kN + 32 + lane); // x_656 .. x_659
     __syncwarp();
 
-    const std::uint32_t* p32 = reinterpret_cast<const std::uint32_t*>(p.polys + (long long)pidx * 312);
+    // coefficients to shared memory (+1 zero word for the look-ahead past bit 19967)
+    __shared__ std::uint32_t p32[kN + 2];
+    {
+        const std::uint32_t* pg = reinterpret_cast<const std::uint32_t*>(p.polys + (long long)pidx * 312);
+        for (int k = lane; k < kN; k += 32)
+            p32[k] = __ldg(pg + k);
+        if (lane < 2)
+            p32[kN + lane] = 0;
+        __syncwarp();
+    }
     std::uint32_t Y[20], A[20], B[20];
 #pragma unroll
     for (int k = 0; k < 20; ++k)
