@@ -17,7 +17,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libvmt19937_b200.so")
 SOURCES = ["vmt_capi.cu", "gf2poly.cpp"]
-HEADERS = ["vmt_kernels.cuh", "gf2poly.hpp"]
+HEADERS = ["vmt_kernels.cuh", "vmt_common.cuh", "vmt_gen.cuh", "vmt_jump.cuh", "gf2poly.hpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -87,47 +87,52 @@ unsigned log2u(unsigned L) {
 using GenFn = void (*)(GenParams);
 
 struct Variant {
-    int id = 0, L = 0, R = 0, VW = 0, NT = 0, SMEM = 0;
+    int id = 0, L = 0, R = 0, VW = 0, W = 0, NT = 0;
+    bool tma = false;
+    int smem[6] = {};
     GenFn fn[6][2] = {};
 };
 
-template <int L, int R, int VW, int MODE>
+template <int L, int R, int VW, int W, bool TMA, int MODE>
 void fill_mode(Variant& v) {
-    v.fn[MODE][0] = vmt_gen_kernel<L, R, VW, MODE, false>;
-    v.fn[MODE][1] = vmt_gen_kernel<L, R, VW, MODE, true>;
+    v.fn[MODE][0] = vmt_gen_kernel<L, R, VW, W, TMA, MODE, false>;
+    v.fn[MODE][1] = vmt_gen_kernel<L, R, VW, W, TMA, MODE, true>;
+    v.smem[MODE] = GenShape<L, R, VW, W, TMA>::template smem<MODE>();
 }
 
-template <int L, int R, int VW>
+template <int L, int R, int VW, int W = 208, bool TMA = false>
 Variant make_variant(int id) {
     Variant v;
     v.id = id;
     v.L = L;
     v.R = R;
     v.VW = VW;
-    v.NT = GenShape<L, R, VW>::NT;
-    v.SMEM = GenShape<L, R, VW>::SMEM;
-    fill_mode<L, R, VW, MODE_U32>(v);
-    fill_mode<L, R, VW, MODE_XOR>(v);
-    fill_mode<L, R, VW, MODE_F32>(v);
-    fill_mode<L, R, VW, MODE_F64>(v);
-    fill_mode<L, R, VW, MODE_F64_REAL3>(v);
-    fill_mode<L, R, VW, MODE_F64_RES53>(v);
+    v.W = W;
+    v.tma = TMA;
+    v.NT = GenShape<L, R, VW, W, TMA>::NT;
+    fill_mode<L, R, VW, W, TMA, MODE_U32>(v);
+    fill_mode<L, R, VW, W, TMA, MODE_XOR>(v);
+    fill_mode<L, R, VW, W, TMA, MODE_F32>(v);
+    fill_mode<L, R, VW, W, TMA, MODE_F64>(v);
+    fill_mode<L, R, VW, W, TMA, MODE_F64_REAL3>(v);
+    fill_mode<L, R, VW, W, TMA, MODE_F64_RES53>(v);
     return v;
 }
 
 // Kernel shape variants (vmt_set_tuning): run length R = consecutive words
-// per thread per window, VW = lanes per thread. The first entry per lane
-// count is the default.
-//   id 1: R=13 VW=4   id 2: R=4 VW=4   id 3: R=13 VW=2   id 4: R=13 VW=1
-//   id 5: R=1 VW=4
+// per thread per window, VW = lanes per thread, W = window, TMA = window
+// output staged in shared memory and written by one bulk copy. The first
+// entry per lane count is the default (DESIGN.md section 4 has the sweep).
+//   id 3: R=13 VW=2   id 1: R=13 VW=4   id 4: R=13 VW=1   id 5: R=1 VW=4
+//   id 6: R=13 VW=2 W=104 TMA bulk stores
 const Variant& pick_variant(unsigned L, int variant) {
     static const std::vector<Variant> table = {
-        make_variant<32, 13, 4>(1), make_variant<32, 4, 4>(2), make_variant<32, 13, 2>(3),
-        make_variant<32, 13, 1>(4),
-        make_variant<16, 13, 4>(1), make_variant<16, 13, 2>(3), make_variant<16, 13, 1>(4),
-        make_variant<16, 1, 4>(5),
-        make_variant<8, 13, 4>(1), make_variant<8, 13, 2>(3), make_variant<8, 13, 1>(4), make_variant<8, 1, 4>(5),
-        make_variant<4, 13, 1>(4), make_variant<4, 1, 4>(5), make_variant<4, 13, 2>(3),
+        make_variant<32, 13, 2>(3), make_variant<32, 13, 4>(1), make_variant<32, 13, 1>(4),
+        make_variant<32, 13, 2, 104, true>(6),
+        make_variant<16, 13, 2>(3), make_variant<16, 13, 4>(1), make_variant<16, 13, 1>(4),
+        make_variant<16, 1, 4>(5), make_variant<16, 13, 2, 104, true>(6),
+        make_variant<8, 13, 2>(3), make_variant<8, 13, 4>(1), make_variant<8, 13, 1>(4), make_variant<8, 1, 4>(5),
+        make_variant<4, 13, 1>(4), make_variant<4, 1, 4>(5),
         make_variant<2, 13, 1>(4), make_variant<2, 1, 2>(5),
         make_variant<1, 1, 1>(5),
     };
@@ -555,7 +560,8 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
               (esz == 4 || V == 4);
     }
     GenFn fn = v.fn[mode][vec ? 1 : 0];
-    const int occ = prepare_gen(h->device, fn, v.NT, v.SMEM);
+    const int smem = v.smem[mode];
+    const int occ = prepare_gen(h->device, fn, v.NT, smem);
     const int sms = device_info(h->device).sms;
     const std::uint64_t max_grid = (std::uint64_t)sms * occ;
     std::uint64_t C = std::max<std::uint64_t>(1, max_grid / groups);
@@ -565,7 +571,7 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     static const bool debug = std::getenv("VMT_DEBUG") != nullptr;
     if (debug)
         std::fprintf(stderr, "[vmt] L=%u R=%d NT=%d smem=%d occ=%d chunks=%llu blocks=%llu mode=%d vec=%d\n", h->L,
-                     v.R, v.NT, v.SMEM, occ, (unsigned long long)C, (unsigned long long)nb, mode, (int)vec);
+                     v.R, v.NT, smem, occ, (unsigned long long)C, (unsigned long long)nb, mode, (int)vec);
     const std::uint64_t B = (nb + C - 1) / C;
     C = (nb + B - 1) / B;
 
@@ -601,7 +607,7 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     p.out_chunk_stride = 0;
     p.blocks_per_chunk = (unsigned)B;
     p.lanes = h->L;
-    fn<<<(unsigned)grid, v.NT, v.SMEM, st>>>(p);
+    fn<<<(unsigned)grid, v.NT, smem, st>>>(p);
     VMT_CUDA(cudaGetLastError());
     h->cnt.gen += 1;
     if (h->profile) {
@@ -1021,7 +1027,7 @@ int vmt_batch_fill_u32(uint32_t seed0, unsigned ngen, unsigned lanes, unsigned j
         }
         const bool vec = (reinterpret_cast<std::uintptr_t>(out) % 16 == 0) && (n_per_gen % 4 == 0);
         GenFn fn = v.fn[MODE_U32][vec ? 1 : 0];
-        prepare_gen(device, fn, v.NT, v.SMEM);
+        prepare_gen(device, fn, v.NT, v.smem[MODE_U32]);
         GenParams p{};
         p.chunk_states = states.p;
         p.out = out;
@@ -1033,7 +1039,7 @@ int vmt_batch_fill_u32(uint32_t seed0, unsigned ngen, unsigned lanes, unsigned j
         p.out_chunk_stride = n_per_gen;
         p.blocks_per_chunk = (unsigned)p.end_block;
         p.lanes = lanes;
-        fn<<<ngen, v.NT, v.SMEM, st>>>(p);
+        fn<<<ngen, v.NT, v.smem[MODE_U32], st>>>(p);
         VMT_CUDA(cudaGetLastError());
         if (!dev)
             VMT_CUDA(cudaMemcpyAsync(dst, scratch.p, (size_t)ngen * n_per_gen * 4, cudaMemcpyDeviceToHost, st));

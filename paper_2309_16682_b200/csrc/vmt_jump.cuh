@@ -1,0 +1,222 @@
+// sm_100a jump-ahead, seeding and reduction kernels (see vmt_common.cuh).
+#pragma once
+
+#include "vmt_common.cuh"
+
+namespace vmt_b200 {
+
+// ---------------------------------------------------------------------------
+// Jump kernel: one warp per job. Job j computes dst_j = poly_j(F) src_j with
+// the convolution y_k = XOR_{i : p_i = 1} x_{i+k} over the word sequence
+// generated from src (x_0..x_623 = src), y_0 keeping only its live bit
+// (mt19937.cpp:79). Thread tau owns output words 20*tau .. 20*tau+19 (the top
+// 16 of lane 31 are discarded) and keeps the 20 sequence words they need in
+// registers; each group of 20 coefficient steps reads the next 20 words with
+// five conflict-free 128-bit shared loads from a 1024-word per-warp sequence
+// ring that lanes 0..19 extend by 20 words per group.
+struct JumpParams {
+    const std::uint32_t* src;
+    std::uint32_t* dst;
+    const std::uint64_t* polys;       // [npoly][312]
+    const long long* job_src;         // word offset of state j in src (nullable: affine map below)
+    const long long* job_dst;         // word offset of state j in dst
+    const int* job_poly;              // poly index of job j
+    int src_stride;                   // word k of a state at offset + k*stride
+    int dst_stride;
+    int njobs;
+    // affine job map when job_src == nullptr: a = j / div, b = j % div
+    int div;
+    long long s_a, s_b, s_c, d_a, d_b, d_c;
+    int p_a, p_b, p_c;
+};
+
+constexpr int kJumpWarps = 1;
+constexpr int kSeqRing = 1024;
+constexpr int kGroups = 998; // 998 * 20 = 19960 >= 19937 coefficient steps
+
+template <int S>
+__device__ __forceinline__ void jump_pair(std::uint32_t (&Y)[20], const std::uint32_t (&A)[20],
+                                          const std::uint32_t (&B)[20], unsigned bits) {
+    // steps S and S+1 of a 20-step group: position k sees x at offset S+k / S+1+k
+    // of the 40-word window A ++ B.
+    if (bits == 3u) {
+#pragma unroll
+        for (int k = 0; k < 20; ++k) {
+            const std::uint32_t v0 = (S + k) < 20 ? A[(S + k) % 20] : B[(S + k) % 20];
+            const std::uint32_t v1 = (S + 1 + k) < 20 ? A[(S + 1 + k) % 20] : B[(S + 1 + k) % 20];
+            Y[k] ^= v0 ^ v1;
+        }
+    } else if (bits == 1u) {
+#pragma unroll
+        for (int k = 0; k < 20; ++k)
+            Y[k] ^= (S + k) < 20 ? A[(S + k) % 20] : B[(S + k) % 20];
+    } else if (bits == 2u) {
+#pragma unroll
+        for (int k = 0; k < 20; ++k)
+            Y[k] ^= (S + 1 + k) < 20 ? A[(S + 1 + k) % 20] : B[(S + 1 + k) % 20];
+    }
+}
+
+__device__ __forceinline__ unsigned poly_bits20(const std::uint32_t* p32, int i) {
+    // 20 coefficient bits starting at bit i (p32 in shared memory)
+    const int w = i >> 5, o = i & 31;
+    const unsigned long long two = ((unsigned long long)p32[w + 1] << 32) | p32[w];
+    return (unsigned)(two >> o) & 0xFFFFFu;
+}
+
+__device__ __forceinline__ void jump_produce(std::uint32_t* seq, int m) {
+    // x_m from x_{m-624}, x_{m-623}, x_{m-227}
+    seq[m & (kSeqRing - 1)] = twist(seq[(m - kN) & (kSeqRing - 1)], seq[(m - kN + 1) & (kSeqRing - 1)],
+                                    seq[(m - kN + kM) & (kSeqRing - 1)]);
+}
+
+__device__ __forceinline__ void jump_load20(const std::uint32_t* seq, int start, std::uint32_t (&B)[20]) {
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+        const uint4 t = *reinterpret_cast<const uint4*>(seq + ((start + 4 * v) & (kSeqRing - 1)));
+        B[4 * v] = t.x;
+        B[4 * v + 1] = t.y;
+        B[4 * v + 2] = t.z;
+        B[4 * v + 3] = t.w;
+    }
+}
+
+// One warp per CTA, so everything derived from the job index (the polynomial
+// coefficients driving the branches) is CTA-uniform.
+#ifndef VMT_JUMP_MINB
+#define VMT_JUMP_MINB 32
+#endif
+__global__ void __launch_bounds__(32, VMT_JUMP_MINB) vmt_jump_kernel(JumpParams p) {
+    __shared__ __align__(16) std::uint32_t seq[kSeqRing];
+    const int lane = threadIdx.x;
+    const int job = blockIdx.x;
+    if (job >= p.njobs)
+        return;
+    long long so, dof;
+    int pidx;
+    if (p.job_src != nullptr) {
+        so = p.job_src[job];
+        dof = p.job_dst[job];
+        pidx = p.job_poly[job];
+    } else {
+        const long long a = job / p.div, b = job % p.div;
+        so = a * p.s_a + b * p.s_b + p.s_c;
+        dof = a * p.d_a + b * p.d_b + p.d_c;
+        pidx = (int)(a * p.p_a + b * p.p_b + p.p_c);
+    }
+    const std::uint32_t* src = p.src + so;
+    for (int k = lane; k < kN; k += 32)
+        seq[k] = src[(long long)k * p.src_stride];
+    __syncwarp();
+    jump_produce(seq, kN + lane); // x_624 .. x_655
+    __syncwarp();
+    if (lane < 4)
+        jump_produce(seq, kN + 32 + lane); // x_656 .. x_659
+    __syncwarp();
+
+    // coefficients to shared memory (+1 zero word for the look-ahead past bit 19967)
+    __shared__ std::uint32_t p32[kN + 2];
+    {
+        const std::uint32_t* pg = reinterpret_cast<const std::uint32_t*>(p.polys + (long long)pidx * 312);
+        for (int k = lane; k < kN; k += 32)
+            p32[k] = __ldg(pg + k);
+        if (lane < 2)
+            p32[kN + lane] = 0;
+        __syncwarp();
+    }
+    std::uint32_t Y[20], A[20], B[20];
+#pragma unroll
+    for (int k = 0; k < 20; ++k)
+        Y[k] = 0;
+    jump_load20(seq, 20 * lane, A);
+    unsigned cm = poly_bits20(p32, 0);
+
+#pragma unroll 1
+    for (int g = 0; g < kGroups; g += 2) {
+        // ---- group g (window A ++ B)
+        {
+            const int i = 20 * g;
+            jump_load20(seq, i + 20 * lane + 20, B);
+            if (lane < 20)
+                jump_produce(seq, i + 660 + lane);
+            const unsigned cn = poly_bits20(p32, i + 20);
+            jump_pair<0>(Y, A, B, cm & 3u);
+            jump_pair<2>(Y, A, B, (cm >> 2) & 3u);
+            jump_pair<4>(Y, A, B, (cm >> 4) & 3u);
+            jump_pair<6>(Y, A, B, (cm >> 6) & 3u);
+            jump_pair<8>(Y, A, B, (cm >> 8) & 3u);
+            jump_pair<10>(Y, A, B, (cm >> 10) & 3u);
+            jump_pair<12>(Y, A, B, (cm >> 12) & 3u);
+            jump_pair<14>(Y, A, B, (cm >> 14) & 3u);
+            jump_pair<16>(Y, A, B, (cm >> 16) & 3u);
+            jump_pair<18>(Y, A, B, (cm >> 18) & 3u);
+            cm = cn;
+            __syncwarp();
+        }
+        // ---- group g+1 (window B ++ A)
+        {
+            const int i = 20 * (g + 1);
+            jump_load20(seq, i + 20 * lane + 20, A);
+            if (lane < 20)
+                jump_produce(seq, i + 660 + lane);
+            const unsigned cn = (g + 2 < kGroups) ? poly_bits20(p32, i + 20) : 0u;
+            jump_pair<0>(Y, B, A, cm & 3u);
+            jump_pair<2>(Y, B, A, (cm >> 2) & 3u);
+            jump_pair<4>(Y, B, A, (cm >> 4) & 3u);
+            jump_pair<6>(Y, B, A, (cm >> 6) & 3u);
+            jump_pair<8>(Y, B, A, (cm >> 8) & 3u);
+            jump_pair<10>(Y, B, A, (cm >> 10) & 3u);
+            jump_pair<12>(Y, B, A, (cm >> 12) & 3u);
+            jump_pair<14>(Y, B, A, (cm >> 14) & 3u);
+            jump_pair<16>(Y, B, A, (cm >> 16) & 3u);
+            jump_pair<18>(Y, B, A, (cm >> 18) & 3u);
+            cm = cn;
+            __syncwarp();
+        }
+    }
+    std::uint32_t* dst = p.dst + dof;
+#pragma unroll
+    for (int k = 0; k < 20; ++k) {
+        const int j = 20 * lane + k;
+        if (j < kN)
+            dst[(long long)j * p.dst_stride] = (j == 0) ? (Y[k] & kUpperMask) : Y[k];
+    }
+}
+
+// init_genrand (mt19937.cpp:22-27): state n = seeds[n] written at
+// dst + n*state_stride + k*word_stride.
+__global__ void vmt_seed_kernel(const std::uint32_t* seeds, int n, std::uint32_t* dst, long long state_stride,
+                                int word_stride) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n)
+        return;
+    std::uint32_t w = seeds[i];
+    std::uint32_t* d = dst + (long long)i * state_stride;
+    d[0] = w;
+    for (std::uint32_t k = 1; k < (std::uint32_t)kN; ++k) {
+        w = 1812433253u * (w ^ (w >> 30)) + k;
+        d[(long long)k * word_stride] = w;
+    }
+}
+
+// XOR-reduce per-CTA (untempered) partials into out[0] and temper the total.
+__global__ void vmt_xor_reduce_kernel(const std::uint32_t* partials, int n, std::uint32_t* out) {
+    std::uint32_t acc = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        acc ^= partials[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        acc ^= __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+    __shared__ std::uint32_t red[32];
+    if ((threadIdx.x & 31) == 0)
+        red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        std::uint32_t x = 0;
+        for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w)
+            x ^= red[w];
+        out[0] = temper(x); // XOR of tempered words == temper(XOR of words)
+    }
+}
+
+} // namespace vmt_b200

@@ -243,3 +243,48 @@ def test_empty_fill_and_host_destination():
     d = dev_u32(10000)
     r.fill_u32(d)
     assert np.array_equal(h, host(d))
+
+
+@pytest.mark.parametrize("L,variants", [(32, [1, 3, 4, 6]), (16, [1, 3, 4, 5, 6]), (8, [1, 3, 4, 5]), (4, [4, 5]),
+                                        (2, [4, 5]), (1, [5])])
+def test_kernel_variants_identical(oracle, L, variants):
+    """Every CTA-shape variant (run length, vector width, window, TMA bulk
+    stores) emits the same words, across chunk boundaries and ragged ends."""
+    q = 10
+    lanes = oracle.dephased_states(2024, L, oracle.x_pow2_mod(q)) if L > 1 else oracle.seed_words(2024)[None]
+    start, n = 3 * 624 * L + 5, 40 * 624 * L + 77
+    ref = oracle.vmt_stream(lanes, start, n)
+    for v in variants:
+        for chunks in (1, 5):
+            g = V.VmtEngine(L, 2024, q)
+            g.set_tuning(max_chunks=chunks, variant=v)
+            g.skip(start)
+            out = dev_u32(n + 8)[4:4 + n]  # 16-byte misaligned destination too
+            g.fill_u32(out)
+            assert np.array_equal(host(out), ref), (L, v, chunks)
+            g2 = V.VmtEngine(L, 2024, q)
+            g2.set_tuning(max_chunks=chunks, variant=v)
+            g2.skip(start)
+            out2 = dev_u32(n)
+            g2.fill_u32(out2)
+            assert np.array_equal(host(out2), ref), (L, v, chunks, "aligned")
+            x = V.VmtEngine(L, 2024, q)
+            x.set_tuning(max_chunks=chunks, variant=v)
+            x.skip(start)
+            assert x.checksum_xor(n) == int(np.bitwise_xor.reduce(ref)), (L, v, chunks, "xor")
+
+
+def test_float_conversions_tma_variant(oracle):
+    L, q, n = 16, 12, 300000
+    lanes = oracle.dephased_states(42, L, oracle.x_pow2_mod(q))
+    u = oracle.vmt_stream(lanes, 0, n)
+    g = V.VmtEngine(L, 42, q)
+    g.set_tuning(variant=6)
+    t = torch.empty(n, dtype=torch.float32, device="cuda")
+    g.fill_f32(t)
+    assert np.array_equal(host(t), (u >> 8).astype(np.float32) * np.float32(2.0 ** -24))
+    g = V.VmtEngine(L, 42, q)
+    g.set_tuning(variant=6)
+    t = torch.empty(n, dtype=torch.float64, device="cuda")
+    g.fill_f64(t)
+    assert np.array_equal(host(t), u.astype(np.float64) * 2.0 ** -32)
