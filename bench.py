@@ -59,6 +59,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--chunks", type=int, default=0)
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="weak: every rank generates its own 2^34-word share of an N*2^34-word stream "
+                         "per step (the path shards with no data exchange); strong: one 2^34 stream "
+                         "split N ways")
     return ap.parse_args()
 
 
@@ -179,7 +183,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": statistics.median(s for _, s in vals) * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded generator)",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded generator)",
         "config": {"workload": "c4: L=32 VMT19937 stream, 2^34 uint32 per step", "total_words": words,
                    "reference_lanes": 16, "reference_jump_exponent": 16,
                    "note": "reference engine supports L<=16 (engine.hpp:43); M=16 AVX-512 engines, q=16 "
@@ -212,7 +216,8 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    T = args.words
+    # T = words the whole job generates per step (all ranks)
+    T = args.words * world if args.scaling == "weak" else args.words
     start, count = partition(T, world, rank)
 
     g = V.VmtGenerator(SEED, V.VmtConfig(LANES), device=local)
@@ -302,13 +307,14 @@ def main():
     traffic = profiled_traffic()
     line = {
         "metric": METRIC, "value": T / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded generator, no inputs)",
         "config": {"workload": "c4: one L=32 VMT19937 stream, seed 5489, default full-period de-phasing "
-                               "(q=19932), 2^34 uint32 per step partitioned across ranks",
+                               "(q=19932), 2^34 uint32 per rank per step (weak) / per step (strong), "
+                               "contiguous per-rank ranges",
                    "total_words": T, "lanes": LANES, "jump_exponent": g.jump_exponent(), "mode": args.mode,
-                   "per_rank_words": count, "l2": "output 64 GiB/N per step >> 126 MB L2 (no flush needed)",
-                   "parallelism": f"stream partition x{world}"},
+                   "per_rank_words": count, "l2": "output >= 8 GiB per rank per step >> 126 MB L2 (no flush)",
+                   "parallelism": f"stream partition x{world} ({args.scaling})"},
         "gpu_launches": launches,
         "per_gpu_value": count / (ms * 1e-3),
         "gen_kernel_ms": gen_ms, "positioning_jump_ms": jump_ms,

@@ -34,6 +34,59 @@ constexpr int kJumpWarps = 1;
 constexpr int kSeqRing = 1024;
 constexpr int kGroups = 998; // 998 * 20 = 19960 >= 19937 coefficient steps
 
+// Four coefficient steps S..S+3 with bit pattern PAT: position k XORs the
+// window words at offsets S+b+k for the set bits b, two per LOP3.
+template <int S, unsigned PAT>
+__device__ __forceinline__ void jump_quad_apply(std::uint32_t (&Y)[20], const std::uint32_t (&A)[20],
+                                                const std::uint32_t (&B)[20]) {
+#pragma unroll
+    for (int k = 0; k < 20; ++k) {
+        std::uint32_t t[4];
+        int n = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+            if ((PAT >> b) & 1u) {
+                const int idx = S + b + k;
+                t[n++] = idx < 20 ? A[idx % 20] : B[idx % 20];
+            }
+        if (n == 1)
+            Y[k] ^= t[0];
+        else if (n == 2)
+            Y[k] ^= t[0] ^ t[1];
+        else if (n == 3)
+            Y[k] = xor3(xor3(Y[k], t[0], t[1]), t[2], 0u);
+        else if (n == 4)
+            Y[k] = xor3(xor3(Y[k], t[0], t[1]), t[2], t[3]);
+    }
+}
+
+template <int S>
+__device__ __forceinline__ void jump_quad(std::uint32_t (&Y)[20], const std::uint32_t (&A)[20],
+                                          const std::uint32_t (&B)[20], unsigned m) {
+    switch (m) {
+    case 1: jump_quad_apply<S, 1>(Y, A, B); break;
+    case 2: jump_quad_apply<S, 2>(Y, A, B); break;
+    case 3: jump_quad_apply<S, 3>(Y, A, B); break;
+    case 4: jump_quad_apply<S, 4>(Y, A, B); break;
+    case 5: jump_quad_apply<S, 5>(Y, A, B); break;
+    case 6: jump_quad_apply<S, 6>(Y, A, B); break;
+    case 7: jump_quad_apply<S, 7>(Y, A, B); break;
+    case 8: jump_quad_apply<S, 8>(Y, A, B); break;
+    case 9: jump_quad_apply<S, 9>(Y, A, B); break;
+    case 10: jump_quad_apply<S, 10>(Y, A, B); break;
+    case 11: jump_quad_apply<S, 11>(Y, A, B); break;
+    case 12: jump_quad_apply<S, 12>(Y, A, B); break;
+    case 13: jump_quad_apply<S, 13>(Y, A, B); break;
+    case 14: jump_quad_apply<S, 14>(Y, A, B); break;
+    case 15: jump_quad_apply<S, 15>(Y, A, B); break;
+    default: break;
+    }
+}
+
+// All 20 steps of a group applied to the window A ++ B.
+__device__ __forceinline__ void jump_group(std::uint32_t (&Y)[20], const std::uint32_t (&A)[20],
+                                           const std::uint32_t (&B)[20], unsigned cm);
+
 template <int S>
 __device__ __forceinline__ void jump_pair(std::uint32_t (&Y)[20], const std::uint32_t (&A)[20],
                                           const std::uint32_t (&B)[20], unsigned bits) {
@@ -55,6 +108,31 @@ __device__ __forceinline__ void jump_pair(std::uint32_t (&Y)[20], const std::uin
         for (int k = 0; k < 20; ++k)
             Y[k] ^= (S + 1 + k) < 20 ? A[(S + 1 + k) % 20] : B[(S + 1 + k) % 20];
     }
+}
+
+#ifndef VMT_JUMP_QUADS
+#define VMT_JUMP_QUADS 0 // 16-way quad switch measured 1.7x slower (code size)
+#endif
+__device__ __forceinline__ void jump_group(std::uint32_t (&Y)[20], const std::uint32_t (&A)[20],
+                                           const std::uint32_t (&B)[20], unsigned cm) {
+#if VMT_JUMP_QUADS
+    jump_quad<0>(Y, A, B, cm & 15u);
+    jump_quad<4>(Y, A, B, (cm >> 4) & 15u);
+    jump_quad<8>(Y, A, B, (cm >> 8) & 15u);
+    jump_quad<12>(Y, A, B, (cm >> 12) & 15u);
+    jump_quad<16>(Y, A, B, (cm >> 16) & 15u);
+#else
+    jump_pair<0>(Y, A, B, cm & 3u);
+    jump_pair<2>(Y, A, B, (cm >> 2) & 3u);
+    jump_pair<4>(Y, A, B, (cm >> 4) & 3u);
+    jump_pair<6>(Y, A, B, (cm >> 6) & 3u);
+    jump_pair<8>(Y, A, B, (cm >> 8) & 3u);
+    jump_pair<10>(Y, A, B, (cm >> 10) & 3u);
+    jump_pair<12>(Y, A, B, (cm >> 12) & 3u);
+    jump_pair<14>(Y, A, B, (cm >> 14) & 3u);
+    jump_pair<16>(Y, A, B, (cm >> 16) & 3u);
+    jump_pair<18>(Y, A, B, (cm >> 18) & 3u);
+#endif
 }
 
 __device__ __forceinline__ unsigned poly_bits20(const std::uint32_t* p32, int i) {
@@ -140,16 +218,7 @@ __global__ void __launch_bounds__(32, VMT_JUMP_MINB) vmt_jump_kernel(JumpParams 
             if (lane < 20)
                 jump_produce(seq, i + 660 + lane);
             const unsigned cn = poly_bits20(p32, i + 20);
-            jump_pair<0>(Y, A, B, cm & 3u);
-            jump_pair<2>(Y, A, B, (cm >> 2) & 3u);
-            jump_pair<4>(Y, A, B, (cm >> 4) & 3u);
-            jump_pair<6>(Y, A, B, (cm >> 6) & 3u);
-            jump_pair<8>(Y, A, B, (cm >> 8) & 3u);
-            jump_pair<10>(Y, A, B, (cm >> 10) & 3u);
-            jump_pair<12>(Y, A, B, (cm >> 12) & 3u);
-            jump_pair<14>(Y, A, B, (cm >> 14) & 3u);
-            jump_pair<16>(Y, A, B, (cm >> 16) & 3u);
-            jump_pair<18>(Y, A, B, (cm >> 18) & 3u);
+            jump_group(Y, A, B, cm);
             cm = cn;
             __syncwarp();
         }
@@ -160,16 +229,7 @@ __global__ void __launch_bounds__(32, VMT_JUMP_MINB) vmt_jump_kernel(JumpParams 
             if (lane < 20)
                 jump_produce(seq, i + 660 + lane);
             const unsigned cn = (g + 2 < kGroups) ? poly_bits20(p32, i + 20) : 0u;
-            jump_pair<0>(Y, B, A, cm & 3u);
-            jump_pair<2>(Y, B, A, (cm >> 2) & 3u);
-            jump_pair<4>(Y, B, A, (cm >> 4) & 3u);
-            jump_pair<6>(Y, B, A, (cm >> 6) & 3u);
-            jump_pair<8>(Y, B, A, (cm >> 8) & 3u);
-            jump_pair<10>(Y, B, A, (cm >> 10) & 3u);
-            jump_pair<12>(Y, B, A, (cm >> 12) & 3u);
-            jump_pair<14>(Y, B, A, (cm >> 14) & 3u);
-            jump_pair<16>(Y, B, A, (cm >> 16) & 3u);
-            jump_pair<18>(Y, B, A, (cm >> 18) & 3u);
+            jump_group(Y, B, A, cm);
             cm = cn;
             __syncwarp();
         }
