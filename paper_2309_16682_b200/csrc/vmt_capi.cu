@@ -87,54 +87,58 @@ unsigned log2u(unsigned L) {
 using GenFn = void (*)(GenParams);
 
 struct Variant {
-    int id = 0, L = 0, R = 0, VW = 0, W = 0, NT = 0;
+    int id = 0, L = 0, G = 0, R = 0, VW = 0, W = 0, NT = 0;
     bool tma = false;
     int smem[6] = {};
     GenFn fn[6][2] = {};
 };
 
-template <int L, int R, int VW, int W, bool TMA, int MODE>
+template <int LT, int G, int R, int VW, int W, bool TMA, int MODE>
 void fill_mode(Variant& v) {
-    v.fn[MODE][0] = vmt_gen_kernel<L, R, VW, W, TMA, MODE, false>;
-    v.fn[MODE][1] = vmt_gen_kernel<L, R, VW, W, TMA, MODE, true>;
-    v.smem[MODE] = GenShape<L, R, VW, W, TMA>::template smem<MODE>();
+    v.fn[MODE][0] = vmt_gen_kernel<LT, G, R, VW, W, TMA, MODE, false>;
+    v.fn[MODE][1] = vmt_gen_kernel<LT, G, R, VW, W, TMA, MODE, true>;
+    v.smem[MODE] = GenShape<G, R, VW, W, TMA>::template smem<MODE>();
 }
 
-template <int L, int R, int VW, int W = 208, bool TMA = false>
+// LT = lanes of the stream, G = lanes per CTA (LT/G CTAs per chunk)
+template <int LT, int G, int R, int VW, int W = 208, bool TMA = false>
 Variant make_variant(int id) {
     Variant v;
     v.id = id;
-    v.L = L;
+    v.L = LT;
+    v.G = G;
     v.R = R;
     v.VW = VW;
     v.W = W;
     v.tma = TMA;
-    v.NT = GenShape<L, R, VW, W, TMA>::NT;
-    fill_mode<L, R, VW, W, TMA, MODE_U32>(v);
-    fill_mode<L, R, VW, W, TMA, MODE_XOR>(v);
-    fill_mode<L, R, VW, W, TMA, MODE_F32>(v);
-    fill_mode<L, R, VW, W, TMA, MODE_F64>(v);
-    fill_mode<L, R, VW, W, TMA, MODE_F64_REAL3>(v);
-    fill_mode<L, R, VW, W, TMA, MODE_F64_RES53>(v);
+    v.NT = GenShape<G, R, VW, W, TMA>::NT;
+    fill_mode<LT, G, R, VW, W, TMA, MODE_U32>(v);
+    fill_mode<LT, G, R, VW, W, TMA, MODE_XOR>(v);
+    fill_mode<LT, G, R, VW, W, TMA, MODE_F32>(v);
+    fill_mode<LT, G, R, VW, W, TMA, MODE_F64>(v);
+    fill_mode<LT, G, R, VW, W, TMA, MODE_F64_REAL3>(v);
+    fill_mode<LT, G, R, VW, W, TMA, MODE_F64_RES53>(v);
     return v;
 }
 
 // Kernel shape variants (vmt_set_tuning): run length R = consecutive words
-// per thread per window, VW = lanes per thread, W = window, TMA = window
-// output staged in shared memory and written by one bulk copy. The first
-// entry per lane count is the default (DESIGN.md section 4 has the sweep).
+// per thread per window, VW = lanes per thread, W = window, G = lanes per
+// CTA, TMA = window output staged in shared memory and written by one bulk
+// copy. The first entry per lane count is the default.
 //   id 3: R=13 VW=2   id 1: R=13 VW=4   id 4: R=13 VW=1   id 5: R=1 VW=4
 //   id 6: R=13 VW=2 W=104 TMA bulk stores
+//   id 7: R=13 VW=2 G=8 (lane groups of 8)   id 8: R=13 VW=2 G=16
 const Variant& pick_variant(unsigned L, int variant) {
     static const std::vector<Variant> table = {
-        make_variant<32, 13, 2>(3), make_variant<32, 13, 4>(1), make_variant<32, 13, 1>(4),
-        make_variant<32, 13, 2, 104, true>(6),
-        make_variant<16, 13, 2>(3), make_variant<16, 13, 4>(1), make_variant<16, 13, 1>(4),
-        make_variant<16, 1, 4>(5), make_variant<16, 13, 2, 104, true>(6),
-        make_variant<8, 13, 2>(3), make_variant<8, 13, 4>(1), make_variant<8, 13, 1>(4), make_variant<8, 1, 4>(5),
-        make_variant<4, 13, 1>(4), make_variant<4, 1, 4>(5),
-        make_variant<2, 13, 1>(4), make_variant<2, 1, 2>(5),
-        make_variant<1, 1, 1>(5),
+        make_variant<32, 32, 13, 2>(3), make_variant<32, 32, 13, 4>(1), make_variant<32, 32, 13, 1>(4),
+        make_variant<32, 32, 13, 2, 104, true>(6), make_variant<32, 8, 13, 2>(7), make_variant<32, 16, 13, 2>(8),
+        make_variant<16, 16, 13, 2>(3), make_variant<16, 16, 13, 4>(1), make_variant<16, 16, 13, 1>(4),
+        make_variant<16, 16, 1, 4>(5), make_variant<16, 16, 13, 2, 104, true>(6), make_variant<16, 8, 13, 2>(7),
+        make_variant<8, 8, 13, 2>(3), make_variant<8, 8, 13, 4>(1), make_variant<8, 8, 13, 1>(4),
+        make_variant<8, 8, 1, 4>(5),
+        make_variant<4, 4, 13, 1>(4), make_variant<4, 4, 1, 4>(5),
+        make_variant<2, 2, 13, 1>(4), make_variant<2, 2, 1, 2>(5),
+        make_variant<1, 1, 1, 1>(5),
     };
     for (const Variant& v : table)
         if (v.L == (int)L && (variant == 0 || v.id == variant))
@@ -316,6 +320,24 @@ struct Counters {
     std::uint64_t gen = 0, jump = 0, other = 0, lane_jumps = 0;
 };
 
+// One CTA per job; with few jobs several warps split each job's coefficient
+// range (vmt_jump.cuh) to cut latency. One warp per job fills an SM with 32.
+void launch_jump_kernel(const JumpParams& jp, cudaStream_t st) {
+    int dev = 0;
+    VMT_CUDA(cudaGetDevice(&dev));
+    const int slots = device_info(dev).sms * 32;
+    const int n = jp.njobs;
+    // measured on B200 (scratch/jump_bench.cu): split 8 wins below ~1/4 of the
+    // warp slots, split 1 from 1/2 upwards
+    if (n >= slots / 2)
+        vmt_jump_kernel<1><<<n, 32, 0, st>>>(jp);
+    else if (n >= slots / 4)
+        vmt_jump_kernel<4><<<n, 128, 0, st>>>(jp);
+    else
+        vmt_jump_kernel<8><<<n, 256, 0, st>>>(jp);
+    VMT_CUDA(cudaGetLastError());
+}
+
 // Launches the jump kernel on jobs (all host vectors; uploaded to dev scratch).
 void launch_jumps(cudaStream_t st, const std::uint32_t* src, int src_stride, std::uint32_t* dst, int dst_stride,
                   const std::uint64_t* d_polys, const std::vector<long long>& jsrc,
@@ -340,8 +362,7 @@ void launch_jumps(cudaStream_t st, const std::uint32_t* src, int src_stride, std
     jp.src_stride = src_stride;
     jp.dst_stride = dst_stride;
     jp.njobs = n;
-    vmt_jump_kernel<<<(n + kJumpWarps - 1) / kJumpWarps, kJumpWarps * 32, 0, st>>>(jp);
-    VMT_CUDA(cudaGetLastError());
+    launch_jump_kernel(jp, st);
     cnt.jump += 1;
     cnt.lane_jumps += n;
     // the job tables are host vectors owned by the caller; make the upload
@@ -378,8 +399,7 @@ void launch_jumps_affine(cudaStream_t st, const std::uint32_t* src, int src_stri
     jp.p_a = a.p_a;
     jp.p_b = a.p_b;
     jp.p_c = a.p_c;
-    vmt_jump_kernel<<<(a.n + kJumpWarps - 1) / kJumpWarps, kJumpWarps * 32, 0, st>>>(jp);
-    VMT_CUDA(cudaGetLastError());
+    launch_jump_kernel(jp, st);
     cnt.jump += 1;
     cnt.lane_jumps += a.n;
 }
@@ -534,6 +554,41 @@ void reposition(vmt_generator* h, std::uint64_t target, cudaStream_t st) {
     h->cur_block = target;
 }
 
+// Chunk count for a fill of n words: every chunk but the first costs L lane
+// jumps (positioning), every chunk adds generation parallelism. Minimise
+//   t(C) = t_jump((C-1) L) + n / min(peak, C * L * r_lane)
+// with constants measured on B200: a lane jump costs
+// 0.43 us of whole-GPU throughput with a latency floor of 0.16-0.5 ms, a
+// lane-state generates ~2.8e8 words/s, the store path saturates at ~1.4e12.
+std::uint64_t plan_chunks(unsigned L, std::uint64_t n, std::uint64_t c_max, int sms) {
+    const double per_jump = 0.43e-6 * 148.0 / (double)sms;
+    auto t_jump = [&](double jobs) -> double {
+        if (jobs <= 0)
+            return 0.0;
+        const double floor_s = jobs <= sms * 4.0 ? 0.16e-3 : (jobs <= sms * 16.0 ? 0.37e-3 : 0.0);
+        return std::max(floor_s, jobs * per_jump);
+    };
+    const double r_lane = 2.8e8, peak = 1.4e12 * (double)sms / 148.0;
+    auto t = [&](std::uint64_t C) {
+        return t_jump(double(C - 1) * L) + double(n) / std::min(peak, double(C) * L * r_lane);
+    };
+    std::uint64_t best = 1;
+    double tb = t(1);
+    for (std::uint64_t C = 2; C <= c_max; C = (C * 5 + 3) / 4) { // ~25% steps
+        const double tc = t(C);
+        if (tc < tb) {
+            tb = tc;
+            best = C;
+        }
+    }
+    if (t(c_max) < tb)
+        best = c_max;
+    // whole waves of one chunk per SM are the sweet spot for large fills
+    if (best > (std::uint64_t)sms && best < c_max && t((std::uint64_t)sms) <= tb * 1.02)
+        best = (std::uint64_t)sms;
+    return best;
+}
+
 // Core: GPU-produces stream words [h->gpos, h->gpos + n) into `out` in the
 // representation of `mode` (out == nullptr only for MODE_XOR). Advances gpos.
 void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaStream_t st, std::uint32_t* xor_out_dev) {
@@ -545,14 +600,14 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     if (h->profile)
         VMT_CUDA(cudaEventRecord(h->ev[0], st));
     const Variant& v = pick_variant(h->L, h->variant);
-    const int groups = 1; // a CTA holds all L lanes of its chunk
+    const int groups = v.L / v.G; // CTAs per chunk (lane groups)
     const std::uint64_t nb = b1 - b0;
     // VEC when the destination is aligned for the vector width: the element
     // of stream word g lives at out + (g - P0).
     const int esz = (mode == MODE_U32 || mode == MODE_F32 || mode == MODE_XOR) ? 4 : 8;
     bool vec = false;
     if (mode != MODE_XOR && mode != MODE_F64_RES53) {
-        const int V = v.L >= v.VW ? v.VW : v.L;
+        const int V = v.G >= v.VW ? v.VW : v.G;
         const std::uintptr_t a = reinterpret_cast<std::uintptr_t>(out);
         const std::uint64_t e = (std::uint64_t)(a / (std::uintptr_t)esz);
         const int need = (esz == 8) ? 2 : V; // double2 / VecT<V> stores
@@ -564,10 +619,8 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     const int occ = prepare_gen(h->device, fn, v.NT, smem);
     const int sms = device_info(h->device).sms;
     const std::uint64_t max_grid = (std::uint64_t)sms * occ;
-    std::uint64_t C = std::max<std::uint64_t>(1, max_grid / groups);
-    if (h->max_chunks)
-        C = std::min<std::uint64_t>(C, h->max_chunks);
-    C = std::min<std::uint64_t>(C, nb);
+    const std::uint64_t c_max = std::min<std::uint64_t>(std::max<std::uint64_t>(1, max_grid / groups), nb);
+    std::uint64_t C = h->max_chunks ? std::min<std::uint64_t>(c_max, h->max_chunks) : plan_chunks(h->L, n, c_max, sms);
     static const bool debug = std::getenv("VMT_DEBUG") != nullptr;
     if (debug)
         std::fprintf(stderr, "[vmt] L=%u R=%d NT=%d smem=%d occ=%d chunks=%llu blocks=%llu mode=%d vec=%d\n", h->L,
@@ -1039,7 +1092,7 @@ int vmt_batch_fill_u32(uint32_t seed0, unsigned ngen, unsigned lanes, unsigned j
         p.out_chunk_stride = n_per_gen;
         p.blocks_per_chunk = (unsigned)p.end_block;
         p.lanes = lanes;
-        fn<<<ngen, v.NT, v.smem[MODE_U32], st>>>(p);
+        fn<<<ngen * (unsigned)(v.L / v.G), v.NT, v.smem[MODE_U32], st>>>(p);
         VMT_CUDA(cudaGetLastError());
         if (!dev)
             VMT_CUDA(cudaMemcpyAsync(dst, scratch.p, (size_t)ngen * n_per_gen * 4, cudaMemcpyDeviceToHost, st));

@@ -195,7 +195,7 @@ struct StageCtl {
 // the run's first p; a: slot of x_{p+397}; wsl: slot receiving x_{p+624}.
 // All ring loads are issued before any ring store (the stores go to slots no
 // thread reads in this window), so the compiler is free to overlap them.
-template <int L, int R, int VW, int W, int MODE, bool VEC, bool FULL, bool STAGE>
+template <int LT, int L, int R, int VW, int W, int MODE, bool VEC, bool FULL, bool STAGE>
 __device__ __forceinline__ void gen_window(std::uint32_t* ring, int base, int a, int wsl, int q, int rho,
                                            unsigned long long g0, const GenParams& p, void* out,
                                            std::uint32_t* acc, StageCtl& sc, int tid) {
@@ -228,7 +228,7 @@ __device__ __forceinline__ void gen_window(std::uint32_t* ring, int base, int a,
             // at the end (vmt_xor_reduce_kernel)
 #pragma unroll
             for (int v = 0; v < V; ++v) {
-                const unsigned long long g = g0 + (unsigned long long)i * L + v;
+                const unsigned long long g = g0 + (unsigned long long)i * LT + v;
                 if (FULL || (g >= p.pos_begin && g < p.pos_end))
                     acc[v] ^= nw[v];
             }
@@ -246,8 +246,8 @@ __device__ __forceinline__ void gen_window(std::uint32_t* ring, int base, int a,
 #pragma unroll
             for (int v = 0; v < V; ++v)
                 tw[v] = temper(nw[v]);
-            emit<MODE, V, VEC, FULL>(tw, g0 + (unsigned long long)i * L, p,
-                                     o + (MODE == MODE_F64_RES53 ? (i * L) / 2 : i * L));
+            emit<MODE, V, VEC, FULL>(tw, g0 + (unsigned long long)i * LT, p,
+                                     o + (MODE == MODE_F64_RES53 ? (i * LT) / 2 : i * LT));
         }
     }
     if (STAGE) {
@@ -281,32 +281,40 @@ __device__ __forceinline__ void gen_window(std::uint32_t* ring, int base, int a,
     }
 }
 
-template <int L, int RING>
+// dst is the stream's [624][LT] state; this CTA's lanes are columns
+// [col0, col0 + L).
+template <int LT, int L, int RING>
 __device__ __forceinline__ void save_boundary(const std::uint32_t* ring, int blk_base_slot, std::uint32_t* dst,
-                                              int tid, int nt) {
+                                              int col0, int tid, int nt) {
     for (int i = tid; i < kN * L; i += nt) {
         const int k = i / L, t = i % L;
         int slot = blk_base_slot + k;
         if (slot >= RING)
             slot -= RING;
-        dst[i] = ring[slot * L + t];
+        dst[(long long)k * LT + col0 + t] = ring[slot * L + t];
     }
 }
 
-// One CTA = one chunk (all L lanes). Dynamic shared memory
-// GenShape::smem<MODE>() bytes: ring[slot][L] | staging[W][L] | mbarrier.
-template <int L, int R, int VW, int W, bool TMA, int MODE, bool VEC>
+// One CTA = one chunk x one group of L of the stream's LT lanes (LT/L CTAs
+// per chunk; L < LT lets more CTAs share an SM for the same lane-state count,
+// i.e. fewer chunks to position). Dynamic shared memory GenShape::smem<MODE>()
+// bytes: ring[slot][L] | staging[W][L] | mbarrier.
+template <int LT, int L, int R, int VW, int W, bool TMA, int MODE, bool VEC>
 __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::NT, GenShape<L, R, VW, W, TMA>::template minb<MODE>())
     vmt_gen_kernel(GenParams p) {
     using S = GenShape<L, R, VW, W, TMA>;
     constexpr int V = S::V;
     using VT = typename VecT<V>::T;
     using E = typename ElemT<MODE>::T;
-    constexpr bool kStaged = VEC && staged_mode<MODE>() && S::template stage_bytes<MODE>() > 0;
+    static_assert(LT % L == 0, "lane groups must tile the stream's lanes");
+    constexpr int kGroups = LT / L;
+    // a window's output is contiguous only when the CTA owns every lane
+    constexpr bool kStaged = VEC && staged_mode<MODE>() && S::template stage_bytes<MODE>() > 0 && kGroups == 1;
     extern __shared__ __align__(16) std::uint32_t ring[];
     __shared__ std::uint32_t red;
 
-    const unsigned chunk = blockIdx.x;
+    const unsigned chunk = blockIdx.x / kGroups;
+    const int col0 = (int)(blockIdx.x % kGroups) * L; // first stream lane of this CTA
     const int tid = threadIdx.x;
     const int q = tid % S::Q;   // vector column (lanes q*V .. q*V+V-1)
     const int rho = tid / S::Q; // run index within a window
@@ -334,9 +342,10 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::NT, GenShape<L, R,
         ((reinterpret_cast<unsigned long long>(out) - p.pos_begin * elem_bytes<MODE>()) % 16ull) == 0;
 
     // -- the chunk's boundary state (words x_0..x_623 -> slots 0..623)
-    const std::uint32_t* src = p.chunk_states + (unsigned long long)chunk * kN * L;
+    const std::uint32_t* src = p.chunk_states + (unsigned long long)chunk * kN * LT + col0;
     for (int i = tid; i < kN * S::Q; i += S::NT) {
-        const VT v = reinterpret_cast<const VT*>(src)[i];
+        const int slot = i / S::Q, qq = i % S::Q;
+        const VT v = *reinterpret_cast<const VT*>(src + (long long)slot * LT + qq * V);
         reinterpret_cast<VT*>(ring)[i] = v;
         if (i < R * S::Q)
             reinterpret_cast<VT*>(ring)[S::RING * S::Q + i] = v;
@@ -352,13 +361,13 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::NT, GenShape<L, R,
 #pragma unroll
     for (int v = 0; v < V; ++v)
         acc[v] = 0;
-    constexpr unsigned long long bw = (unsigned long long)kN * L;
-    constexpr unsigned long long ww = (unsigned long long)W * L; // words per window
+    constexpr unsigned long long bw = (unsigned long long)kN * LT;
+    constexpr unsigned long long ww = (unsigned long long)W * LT; // stream words per window (all lanes)
     const bool save_here = p.save_state != nullptr && (!batch || chunk == 0);
     int blk_base_slot = 0; // slot of x_{624 r} for the current block r (= 624 r mod RING)
     for (unsigned long long blk = b_lo; blk < b_hi; ++blk) {
         if (save_here && blk == p.save_block)
-            save_boundary<L, S::RING>(ring, blk_base_slot, p.save_state, tid, S::NT);
+            save_boundary<LT, L, S::RING>(ring, blk_base_slot, p.save_state, col0, tid, S::NT);
 #pragma unroll 1
         for (int wi = 0; wi < kN / W; ++wi) {
             int wstart = blk_base_slot + wi * W;
@@ -372,18 +381,18 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::NT, GenShape<L, R,
             if (wsl >= S::RING)
                 wsl -= S::RING;
             const unsigned long long gw = blk * bw + (unsigned long long)wi * ww; // first word of the window
-            const unsigned long long g0 = gw + (unsigned long long)(rho * R) * L + q * V;
+            const unsigned long long g0 = gw + (unsigned long long)(rho * R) * LT + col0 + q * V;
             const bool wfull = gw >= p.pos_begin && gw + ww <= p.pos_end;
             const bool staged = kStaged && tma_ok && wfull;
             if (staged)
-                gen_window<L, R, VW, W, MODE, VEC, true, kStaged>(ring, base, a, wsl, q, rho, g0, p, out, acc, sc,
-                                                                  tid);
+                gen_window<LT, L, R, VW, W, MODE, VEC, true, kStaged>(ring, base, a, wsl, q, rho, g0, p, out, acc,
+                                                                      sc, tid);
             else if (wfull)
-                gen_window<L, R, VW, W, MODE, VEC, true, false>(ring, base, a, wsl, q, rho, g0, p, out, acc, sc,
-                                                                tid);
+                gen_window<LT, L, R, VW, W, MODE, VEC, true, false>(ring, base, a, wsl, q, rho, g0, p, out, acc, sc,
+                                                                    tid);
             else
-                gen_window<L, R, VW, W, MODE, VEC, false, false>(ring, base, a, wsl, q, rho, g0, p, out, acc, sc,
-                                                                 tid);
+                gen_window<LT, L, R, VW, W, MODE, VEC, false, false>(ring, base, a, wsl, q, rho, g0, p, out, acc,
+                                                                     sc, tid);
             __syncthreads();
             if (kStaged) {
                 if (staged && tid == 0) {
@@ -404,7 +413,7 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::NT, GenShape<L, R,
     }
     // end-of-range boundary state (block b_hi) when it is the requested one
     if (save_here && b_hi == p.save_block && b_hi == p.end_block)
-        save_boundary<L, S::RING>(ring, blk_base_slot, p.save_state, tid, S::NT);
+        save_boundary<LT, L, S::RING>(ring, blk_base_slot, p.save_state, col0, tid, S::NT);
     if (kStaged && tid == 0 && sc.pending)
         bulk_wait_all(); // the staging buffer must outlive the last bulk copy
     if (kFold) {

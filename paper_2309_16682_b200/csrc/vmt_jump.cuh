@@ -135,11 +135,25 @@ __device__ __forceinline__ void jump_group(std::uint32_t (&Y)[20], const std::ui
 #endif
 }
 
+#ifndef VMT_JUMP_UNIFORM
+#define VMT_JUMP_UNIFORM 1
+#endif
+#ifndef VMT_JUMP_SINGLE_BODY
+#define VMT_JUMP_SINGLE_BODY 0
+#endif
 __device__ __forceinline__ unsigned poly_bits20(const std::uint32_t* p32, int i) {
     // 20 coefficient bits starting at bit i (p32 in shared memory)
     const int w = i >> 5, o = i & 31;
     const unsigned long long two = ((unsigned long long)p32[w + 1] << 32) | p32[w];
-    return (unsigned)(two >> o) & 0xFFFFFu;
+    const unsigned v = (unsigned)(two >> o) & 0xFFFFFu;
+#if VMT_JUMP_UNIFORM
+    // every lane holds the same value; REDUX.OR moves it into a uniform
+    // register so the per-pair bit tests and branches run on the uniform
+    // datapath instead of the vector ALU
+    return __reduce_or_sync(0xFFFFFFFFu, v);
+#else
+    return v;
+#endif
 }
 
 __device__ __forceinline__ void jump_produce(std::uint32_t* seq, int m) {
@@ -159,17 +173,23 @@ __device__ __forceinline__ void jump_load20(const std::uint32_t* seq, int start,
     }
 }
 
-// One warp per CTA, so everything derived from the job index (the polynomial
-// coefficients driving the branches) is CTA-uniform.
+// One job per CTA, so everything derived from the job index (the polynomial
+// coefficients driving the branches) is CTA-uniform. SPLIT warps share a job:
+// warp w takes the w-th slice of the coefficient groups (after advancing its
+// own copy of the sequence to the slice start) and the partial results are
+// XOR-reduced through shared memory -- SPLIT > 1 trades ~10% extra work for a
+// SPLIT-fold shorter latency when there are few jobs.
 #ifndef VMT_JUMP_MINB
 #define VMT_JUMP_MINB 32
 #endif
-__global__ void __launch_bounds__(32, VMT_JUMP_MINB) vmt_jump_kernel(JumpParams p) {
-    __shared__ __align__(16) std::uint32_t seq[kSeqRing];
-    const int lane = threadIdx.x;
+template <int SPLIT>
+__global__ void __launch_bounds__(32 * SPLIT, (SPLIT == 1 ? VMT_JUMP_MINB : 32 / SPLIT)) vmt_jump_kernel(JumpParams p) {
+    __shared__ __align__(16) std::uint32_t seq_all[SPLIT][kSeqRing];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int job = blockIdx.x;
     if (job >= p.njobs)
         return;
+    std::uint32_t* seq = seq_all[warp];
     long long so, dof;
     int pidx;
     if (p.job_src != nullptr) {
@@ -186,31 +206,41 @@ __global__ void __launch_bounds__(32, VMT_JUMP_MINB) vmt_jump_kernel(JumpParams 
     for (int k = lane; k < kN; k += 32)
         seq[k] = src[(long long)k * p.src_stride];
     __syncwarp();
-    jump_produce(seq, kN + lane); // x_624 .. x_655
-    __syncwarp();
-    if (lane < 4)
-        jump_produce(seq, kN + 32 + lane); // x_656 .. x_659
-    __syncwarp();
+    // this warp's coefficient groups [g_lo, g_hi) (even bounds: the loop
+    // below handles groups in pairs)
+    constexpr int kPer = ((kGroups / 2 + SPLIT - 1) / SPLIT) * 2;
+    const int g_lo = warp * kPer;
+    const int g_hi = g_lo + kPer < kGroups ? g_lo + kPer : kGroups;
+    // extend the sequence to x_{20*g_lo + 659} (32 independent words per batch)
+    const int last = 20 * g_lo + 659;
+    for (int m0 = kN; m0 <= last; m0 += 32) {
+        if (m0 + lane <= last)
+            jump_produce(seq, m0 + lane);
+        __syncwarp();
+    }
 
     // coefficients to shared memory (+1 zero word for the look-ahead past bit 19967)
     __shared__ std::uint32_t p32[kN + 2];
     {
         const std::uint32_t* pg = reinterpret_cast<const std::uint32_t*>(p.polys + (long long)pidx * 312);
-        for (int k = lane; k < kN; k += 32)
+        for (int k = threadIdx.x; k < kN; k += 32 * SPLIT)
             p32[k] = __ldg(pg + k);
-        if (lane < 2)
-            p32[kN + lane] = 0;
-        __syncwarp();
+        if (threadIdx.x < 2)
+            p32[kN + threadIdx.x] = 0;
+        if (SPLIT == 1)
+            __syncwarp();
+        else
+            __syncthreads();
     }
     std::uint32_t Y[20], A[20], B[20];
 #pragma unroll
     for (int k = 0; k < 20; ++k)
         Y[k] = 0;
-    jump_load20(seq, 20 * lane, A);
-    unsigned cm = poly_bits20(p32, 0);
+    jump_load20(seq, 20 * g_lo + 20 * lane, A);
+    unsigned cm = g_lo < g_hi ? poly_bits20(p32, 20 * g_lo) : 0u;
 
 #pragma unroll 1
-    for (int g = 0; g < kGroups; g += 2) {
+    for (int g = g_lo; g < g_hi; g += 2) {
         // ---- group g (window A ++ B)
         {
             const int i = 20 * g;
@@ -228,18 +258,34 @@ __global__ void __launch_bounds__(32, VMT_JUMP_MINB) vmt_jump_kernel(JumpParams 
             jump_load20(seq, i + 20 * lane + 20, A);
             if (lane < 20)
                 jump_produce(seq, i + 660 + lane);
-            const unsigned cn = (g + 2 < kGroups) ? poly_bits20(p32, i + 20) : 0u;
+            const unsigned cn = (g + 2 < g_hi) ? poly_bits20(p32, i + 20) : 0u;
             jump_group(Y, B, A, cm);
             cm = cn;
             __syncwarp();
         }
     }
     std::uint32_t* dst = p.dst + dof;
+    if (SPLIT == 1) {
 #pragma unroll
-    for (int k = 0; k < 20; ++k) {
-        const int j = 20 * lane + k;
-        if (j < kN)
-            dst[(long long)j * p.dst_stride] = (j == 0) ? (Y[k] & kUpperMask) : Y[k];
+        for (int k = 0; k < 20; ++k) {
+            const int j = 20 * lane + k;
+            if (j < kN)
+                dst[(long long)j * p.dst_stride] = (j == 0) ? (Y[k] & kUpperMask) : Y[k];
+        }
+    } else {
+        // XOR the warps' partial sums (the sequence rings are free now)
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 20; ++k)
+            seq[20 * lane + k] = Y[k];
+        __syncthreads();
+        for (int j = threadIdx.x; j < kN; j += 32 * SPLIT) {
+            std::uint32_t v = 0;
+#pragma unroll
+            for (int w = 0; w < SPLIT; ++w)
+                v ^= seq_all[w][j];
+            dst[(long long)j * p.dst_stride] = (j == 0) ? (v & kUpperMask) : v;
+        }
     }
 }
 

@@ -245,7 +245,7 @@ def test_empty_fill_and_host_destination():
     assert np.array_equal(h, host(d))
 
 
-@pytest.mark.parametrize("L,variants", [(32, [1, 3, 4, 6]), (16, [1, 3, 4, 5, 6]), (8, [1, 3, 4, 5]), (4, [4, 5]),
+@pytest.mark.parametrize("L,variants", [(32, [1, 3, 4, 6, 7, 8]), (16, [1, 3, 4, 5, 6, 7]), (8, [1, 3, 4, 5]), (4, [4, 5]),
                                         (2, [4, 5]), (1, [5])])
 def test_kernel_variants_identical(oracle, L, variants):
     """Every CTA-shape variant (run length, vector width, window, TMA bulk
