@@ -258,22 +258,46 @@ def main():
     ms = max_over_ranks(ms, dev)
     launches = sum(s1[k] - s0[k] for k in ("gen_launches", "jump_launches", "other_launches"))
 
-    # -- generation kernel alone (CUDA events around it on the same stream)
-    g.set_profiling(True)
-    jumps, gens = [], []
-    for _ in range(args.steps):
-        step()
-        j, gm = g.last_timings()
-        jumps.append(j)
-        gens.append(gm)
-    g.set_profiling(False)
-    gen_ms = max_over_ranks(statistics.mean(gens), dev)
-    jump_ms = max_over_ranks(statistics.mean(jumps), dev)
+    # -- the generation kernel's own duration (CUDA events around it on its
+    # stream): in situ (as in the timed loop: the next step's positioning
+    # jumps run concurrently on a side stream) and isolated (prefetch off:
+    # positioning jumps and generation back to back)
+    def kernel_times():
+        g.set_profiling(True)
+        jumps, gens = [], []
+        for _ in range(args.steps):
+            step()
+            j, gm = g.last_timings()
+            jumps.append(j)
+            gens.append(gm)
+        g.set_profiling(False)
+        return max_over_ranks(statistics.mean(gens), dev), max_over_ranks(statistics.mean(jumps), dev)
+
+    gen_ms, jump_wait_ms = kernel_times()
+    g.set_prefetch(False)
+    step()
+    gen_iso_ms, jump_ms = kernel_times()
+    g.set_prefetch(True)
 
     # -- global checksum of one full 2^34 range (config 4 verification)
     g.seek(start)
     csum = combine_xor(g.checksum_xor(count), dev)
     torch.cuda.synchronize(dev)
+
+    # -- end to end, fused consumer: the step's result is the 4-byte XOR
+    # checksum read back to the host (config 4's no-store mode)
+    g.seek(start)
+    g.checksum_xor(count)
+    g.skip(T - count)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        g.checksum_xor(count)
+        g.skip(T - count)
+    xs = max_over_ranks((time.perf_counter() - t0) / args.steps, dev)
+    e2e_xor = {"value": T / xs, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 4 * world,
+               "ms_per_step": xs * 1e3, "mode": "fused XOR checksum, nothing stored"}
 
     # -- end to end into pinned host memory through the public API
     e2e = None
@@ -304,6 +328,7 @@ def main():
     peak, peak_src = measured_peak()
     bytes_per_launch = count * 4
     achieved = bytes_per_launch / (gen_ms * 1e-3) / 1e9
+    achieved_iso = bytes_per_launch / (gen_iso_ms * 1e-3) / 1e9
     traffic = profiled_traffic()
     line = {
         "metric": METRIC, "value": T / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -317,15 +342,19 @@ def main():
                    "parallelism": f"stream partition x{world} ({args.scaling})"},
         "gpu_launches": launches,
         "per_gpu_value": count / (ms * 1e-3),
-        "gen_kernel_ms": gen_ms, "positioning_jump_ms": jump_ms,
-        "gen_only_value": T / (max(gen_ms, 1e-9) * 1e-3) if world == 1 else None,
+        "timing_breakdown_ms": {"gen_kernel_in_situ": gen_ms, "positioning_wait_in_situ": jump_wait_ms,
+                                "gen_kernel_isolated": gen_iso_ms, "positioning_jumps_isolated": jump_ms,
+                                "note": "in situ = as timed (next step's positioning prefetched on a side "
+                                        "stream, overlapping generation); isolated = prefetch off"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": (traffic or {}).get("dram_bytes_per_launch"),
-                     "kernel": "vmt_gen_kernel", "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": bytes_per_launch},
+                     "kernel": "vmt_gen_kernel (in situ)", "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": bytes_per_launch,
+                     "achieved_isolated": achieved_iso, "frac_isolated": achieved_iso / peak},
         "checksum_xor": f"0x{csum:08x}",
         "clocks": clk,
         "e2e": e2e,
+        "e2e_xor": e2e_xor,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:

@@ -242,6 +242,9 @@ class VmtGenerator:
     def set_tuning(self, max_chunks: int = 0, variant: int = 0) -> None:
         check(lib.vmt_set_tuning(self._h, max_chunks, variant))
 
+    def set_prefetch(self, enable: bool = True) -> None:
+        check(lib.vmt_set_prefetch(self._h, int(enable)))
+
     def set_profiling(self, enable: bool = True) -> None:
         check(lib.vmt_set_profiling(self._h, int(enable)))
 

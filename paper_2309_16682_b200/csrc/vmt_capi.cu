@@ -73,6 +73,8 @@ int guarded(F&& f) {
 // Host-destination fills are staged through device memory in segments of
 // this many stream words (two segments in flight).
 constexpr std::uint64_t kHostSegmentWords = 1ull << 28;
+// Fills at least this large prefetch the positioning of the predicted next fill.
+constexpr std::uint64_t kPrefetchMinWords = 1ull << 24;
 
 bool valid_lanes(unsigned L) { return L == 1 || L == 2 || L == 4 || L == 8 || L == 16 || L == 32; }
 
@@ -424,6 +426,13 @@ struct vmt_generator {
     std::uint64_t gpos = 0; // words produced by the GPU (>= pos)
 
     DevBuf<std::uint32_t> chunks;    // [C][624][L]
+    DevBuf<std::uint32_t> chunks_alt; // prefetched chunk states of the predicted next fill
+    bool prefetch = true;            // position the predicted next fill while this one generates
+    bool pref_valid = false;
+    std::uint64_t pref_b0 = 0, pref_B = 0, pref_C = 0;
+    std::uint64_t last_end = ~0ull;  // end position of the previous GPU fill
+    cudaStream_t side = nullptr;     // prefetch stream
+    cudaEvent_t ev_chunks = nullptr, ev_pref = nullptr;
     DevBuf<std::uint32_t> partials;  // per-CTA xor partials
     DevBuf<std::uint32_t> scratch;   // device staging for host destinations
     DevBuf<std::uint64_t> tmp_poly;
@@ -515,7 +524,29 @@ const std::uint64_t* chunk_polys(vmt_generator* h, std::uint64_t B, size_t C, cu
     return ps.dev.p;
 }
 
-// Moves h->cur (block cur_block) to block `target` (>= cur_block) by one jump.
+// x^(624*delta) mod P on the device, cached per block distance (repeated
+// strides are common: consecutive fills, ranks skipping the other ranks'
+// shares, seeking back to a range).
+const std::uint64_t* skip_poly(vmt_generator* h, std::uint64_t delta) {
+    auto it = h->skipcache.find(delta);
+    if (it == h->skipcache.end()) {
+        if (h->skipcache.size() >= 16)
+            h->skipcache.clear(); // cudaFree synchronises: no in-flight user
+        Gf2Field& F = Gf2Field::instance();
+        // 624*delta may exceed 64 bits for huge skips
+        const unsigned __int128 d = (unsigned __int128)624u * delta;
+        const Poly poly = F.x_pow128((std::uint64_t)d, (std::uint64_t)(d >> 64));
+        auto& slot = h->skipcache[delta];
+        slot.reset(new DevBuf<std::uint64_t>());
+        slot->reserve(kPolyWords);
+        VMT_CUDA(cudaMemcpy(slot->p, poly.data(), kPolyWords * 8, cudaMemcpyHostToDevice));
+        it = h->skipcache.find(delta);
+    }
+    return it->second->p;
+}
+
+// Moves h->cur (block cur_block) to block `target` by one jump (forward from
+// cur, or from the block-0 states when going backwards).
 void reposition(vmt_generator* h, std::uint64_t target, cudaStream_t st) {
     if (target == h->cur_block)
         return;
@@ -527,23 +558,7 @@ void reposition(vmt_generator* h, std::uint64_t target, cudaStream_t st) {
         from = h->base.p;
         delta = target;
     }
-    // x^(624*delta) mod P, cached per distance (repeated strides are common:
-    // a rank skipping the other ranks' shares, or seeking back to a range)
-    auto it = h->skipcache.find(delta);
-    if (it == h->skipcache.end()) {
-        if (h->skipcache.size() >= 16)
-            h->skipcache.clear();
-        Gf2Field& F = Gf2Field::instance();
-        // 624*delta may exceed 64 bits for huge skips
-        const unsigned __int128 d = (unsigned __int128)624u * delta;
-        const Poly poly = F.x_pow128((std::uint64_t)d, (std::uint64_t)(d >> 64));
-        auto& slot = h->skipcache[delta];
-        slot.reset(new DevBuf<std::uint64_t>());
-        slot->reserve(kPolyWords);
-        VMT_CUDA(cudaMemcpy(slot->p, poly.data(), kPolyWords * 8, cudaMemcpyHostToDevice));
-        it = h->skipcache.find(delta);
-    }
-    const std::uint64_t* dp = it->second->p;
+    const std::uint64_t* dp = skip_poly(h, delta);
     AffineJobs a;
     a.n = (int)h->L;
     a.div = (int)h->L;
@@ -628,19 +643,52 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     const std::uint64_t B = (nb + C - 1) / C;
     C = (nb + B - 1) / B;
 
-    h->chunks.reserve((size_t)C * kN * h->L);
-    VMT_CUDA(cudaMemcpyAsync(h->chunks.p, h->cur.p, (size_t)kN * h->L * 4, cudaMemcpyDeviceToDevice, st));
-    if (C > 1) {
-        const std::uint64_t* dp = chunk_polys(h, B, C, st);
-        AffineJobs a;
-        a.n = (int)((C - 1) * h->L);
-        a.div = (int)h->L;
-        a.s_b = 1;
-        a.d_a = (long long)kN * h->L;
-        a.d_b = 1;
-        a.d_c = (long long)kN * h->L;
-        a.p_a = 1;
-        launch_jumps_affine(st, h->cur.p, (int)h->L, h->chunks.p, (int)h->L, dp, a, h->cnt);
+    // -- chunk start states: prefetched during the previous fill, or jumped now
+    const bool use_pref = h->pref_valid && h->pref_b0 == b0 && h->pref_B == B && h->pref_C == C;
+    h->pref_valid = false;
+    if (use_pref) {
+        VMT_CUDA(cudaStreamWaitEvent(st, h->ev_pref, 0));
+        h->chunks.swap(h->chunks_alt);
+    } else {
+        h->chunks.reserve((size_t)C * kN * h->L);
+        VMT_CUDA(cudaMemcpyAsync(h->chunks.p, h->cur.p, (size_t)kN * h->L * 4, cudaMemcpyDeviceToDevice, st));
+        if (C > 1) {
+            const std::uint64_t* dp = chunk_polys(h, B, C, st);
+            AffineJobs a;
+            a.n = (int)((C - 1) * h->L);
+            a.div = (int)h->L;
+            a.s_b = 1;
+            a.d_a = (long long)kN * h->L;
+            a.d_b = 1;
+            a.d_c = (long long)kN * h->L;
+            a.p_a = 1;
+            launch_jumps_affine(st, h->cur.p, (int)h->L, h->chunks.p, (int)h->L, dp, a, h->cnt);
+        }
+    }
+    // -- predict the next fill (same size, same gap) and position its chunks
+    // on the side stream while this fill's generation kernel runs: chunk c of
+    // the next fill is chunk c of this one advanced by the same block delta
+    bool prefetch_now = false;
+    std::uint64_t next_b0 = 0;
+    if (h->prefetch && C > 1 && n >= kPrefetchMinWords) {
+        const std::uint64_t gap = (h->last_end != ~0ull && P0 >= h->last_end) ? P0 - h->last_end : 0;
+        const std::uint64_t P0n = P1 + gap;
+        next_b0 = P0n / h->bw;
+        const std::uint64_t nbn = (P0n + n + h->bw - 1) / h->bw - next_b0;
+        const std::uint64_t c_max_n = std::min<std::uint64_t>(std::max<std::uint64_t>(1, max_grid / groups), nbn);
+        std::uint64_t Cn = h->max_chunks ? std::min<std::uint64_t>(c_max_n, h->max_chunks)
+                                         : plan_chunks(h->L, n, c_max_n, sms);
+        const std::uint64_t Bn = (nbn + Cn - 1) / Cn;
+        Cn = (nbn + Bn - 1) / Bn;
+        prefetch_now = Cn == C && Bn == B && next_b0 >= b0;
+    }
+    if (prefetch_now) {
+        if (!h->side) {
+            VMT_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+            VMT_CUDA(cudaEventCreateWithFlags(&h->ev_chunks, cudaEventDisableTiming));
+            VMT_CUDA(cudaEventCreateWithFlags(&h->ev_pref, cudaEventDisableTiming));
+        }
+        VMT_CUDA(cudaEventRecord(h->ev_chunks, st));
     }
     const std::uint64_t grid = C * groups;
     if (h->profile)
@@ -663,6 +711,27 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     fn<<<(unsigned)grid, v.NT, smem, st>>>(p);
     VMT_CUDA(cudaGetLastError());
     h->cnt.gen += 1;
+    if (prefetch_now) {
+        // launched after the generation kernel so its CTAs take the resources
+        // the generation wave leaves free on every SM
+        const std::uint64_t* dp = skip_poly(h, next_b0 - b0);
+        h->chunks_alt.reserve((size_t)C * kN * h->L);
+        VMT_CUDA(cudaStreamWaitEvent(h->side, h->ev_chunks, 0));
+        AffineJobs a;
+        a.n = (int)(C * h->L);
+        a.div = (int)h->L;
+        a.s_a = (long long)kN * h->L;
+        a.s_b = 1;
+        a.d_a = (long long)kN * h->L;
+        a.d_b = 1;
+        launch_jumps_affine(h->side, h->chunks.p, (int)h->L, h->chunks_alt.p, (int)h->L, dp, a, h->cnt);
+        VMT_CUDA(cudaEventRecord(h->ev_pref, h->side));
+        h->pref_valid = true;
+        h->pref_b0 = next_b0;
+        h->pref_B = B;
+        h->pref_C = C;
+    }
+    h->last_end = P1;
     if (h->profile) {
         VMT_CUDA(cudaEventRecord(h->ev[2], st));
         h->ev_valid = true;
@@ -877,6 +946,12 @@ int vmt_destroy(vmt_handle h) {
             for (auto& e : h->ev)
                 if (e)
                     cudaEventDestroy(e);
+            if (h->side) {
+                cudaStreamSynchronize(h->side);
+                cudaStreamDestroy(h->side);
+                cudaEventDestroy(h->ev_chunks);
+                cudaEventDestroy(h->ev_pref);
+            }
             if (h->copy_stream) {
                 cudaStreamSynchronize(h->copy_stream);
                 cudaStreamDestroy(h->copy_stream);
@@ -1204,6 +1279,15 @@ int vmt_set_tuning(vmt_handle h, unsigned max_chunks, int variant) {
         (void)pick_variant(h->L, variant); // validates
         h->max_chunks = max_chunks;
         h->variant = variant;
+        h->pref_valid = false;
+    });
+}
+
+int vmt_set_prefetch(vmt_handle h, int enable) {
+    return guarded([&] {
+        require(h != nullptr, VMT_EINVAL, "null handle");
+        h->prefetch = enable != 0;
+        h->pref_valid = false;
     });
 }
 

@@ -274,6 +274,29 @@ def test_kernel_variants_identical(oracle, L, variants):
             assert x.checksum_xor(n) == int(np.bitwise_xor.reduce(ref)), (L, v, chunks, "xor")
 
 
+def test_prefetched_positioning_matches(oracle):
+    """Consecutive large fills reuse chunk states prefetched during the
+    previous fill (same size, same gap); mispredictions fall back. The words
+    must be identical to the oracle either way."""
+    L, q = 16, 8
+    lanes = oracle.dephased_states(77, L, oracle.x_pow2_mod(q))
+    n, gap = (1 << 24) + 3, 12345
+    plan = [(n, 0), (n, 0), (n, gap), (n, gap), (n - 7, 0), (n, 0)]
+    pos = 0
+    g = V.VmtEngine(L, 77, q)
+    for i, (size, skip) in enumerate(plan):
+        g.skip(skip)
+        pos += skip
+        out = dev_u32(size)
+        g.fill_u32(out)
+        v = host(out)
+        assert int(np.bitwise_xor.reduce(v)) == oracle.vmt_checksum(lanes, pos, size), i
+        assert np.array_equal(v[:1000], oracle.vmt_stream(lanes, pos, 1000)), i
+        pos += size
+    st = g.stats()
+    assert st["jump_launches"] >= 3
+
+
 def test_float_conversions_tma_variant(oracle):
     L, q, n = 16, 12, 300000
     lanes = oracle.dephased_states(42, L, oracle.x_pow2_mod(q))
