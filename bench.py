@@ -68,52 +68,98 @@ def parse():
 
 # ----------------------------------------------------------------- clocks --
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed
+    region: an NVML poller thread every 5 ms (the timed region of a default
+    run is well under a second, too short for `nvidia-smi -lms`), with the
+    recipe's nvidia-smi query as the fallback when NVML is unusable."""
 
+    # nvmlClocksEventReason* bits
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80}
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
-        self.index = index
-        self.rows = []
+    def __init__(self, device):
+        self.device = device
+        self.rows = []  # (sm_mhz, max_mhz, reasons bitmask)
+        self.src = None
         self.proc = None
+        self.stop_flag = threading.Event()
+        self.nv = None
+        self.handle = None
+        try:
+            import pynvml as nv
+            import torch
+            nv.nvmlInit()
+            uuid = str(torch.cuda.get_device_properties(device).uuid)
+            try:
+                self.handle = nv.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+            except Exception:
+                self.handle = nv.nvmlDeviceGetHandleByIndex(torch.device(device).index or 0)
+            self.nv = nv
+        except Exception:
+            self.nv = None
+
+    def _poll(self):
+        nv, h = self.nv, self.handle
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while True:
+            self.rows.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)), float(mx), int(get_reasons(h))))
+            if self.stop_flag.wait(0.005):
+                break
 
     def start(self):
+        if self.nv is not None:
+            self.src = "nvml (5 ms)"
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return
         try:
+            self.src = "nvidia-smi -lms 100"
+            idx = getattr(self.device, "index", None) or 0
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                ["nvidia-smi", "-i", str(idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread = threading.Thread(target=self._read_smi, daemon=True)
             self.thread.start()
         except Exception:
             self.proc = None
+            self.src = None
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
-
-    def stop(self) -> dict:
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except Exception:
-            self.proc.kill()
-        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+    def _read_smi(self):
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            if len(r) < 8:
+        for line in self.proc.stdout:
+            r = [x.strip() for x in line.split(",")]
+            if len(r) < 8 or not r[0].replace(".", "").isdigit():
                 continue
+            bits = 0
             for i, nm in enumerate(names):
                 if r[4 + i].lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                    bits |= self.BITS[nm]
+            self.rows.append((float(r[0]), float(r[1]) if r[1].replace(".", "").isdigit() else 0.0, bits))
+
+    def stop(self) -> dict:
+        if self.src is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"], "samples": 0}
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        else:
+            self.stop_flag.set()
+            self.thread.join(timeout=2)
+        rows = list(self.rows)
+        reasons = sorted({nm for _, _, bits in rows for nm, b in self.BITS.items() if bits & b})
+        return {"sm_mhz": statistics.median(r[0] for r in rows) if rows else None,
+                "sm_max_mhz": max(r[1] for r in rows) if rows else None,
+                "sm_min_mhz": min(r[0] for r in rows) if rows else None,
+                "reasons": reasons, "samples": len(rows), "source": self.src}
 
 
 def measured_peak():
@@ -240,7 +286,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize(dev)
 
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(dev)
     clocks.start()
     s0 = g.stats()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -258,10 +304,8 @@ def main():
     ms = max_over_ranks(ms, dev)
     launches = sum(s1[k] - s0[k] for k in ("gen_launches", "jump_launches", "other_launches"))
 
-    # -- the generation kernel's own duration (CUDA events around it on its
-    # stream): in situ (as in the timed loop: the next step's positioning
-    # jumps run concurrently on a side stream) and isolated (prefetch off:
-    # positioning jumps and generation back to back)
+    # -- the generation kernel's own duration and the positioning jumps before
+    # it (CUDA events around each on the fill's stream, same steps as timed)
     def kernel_times():
         g.set_profiling(True)
         jumps, gens = [], []
@@ -273,11 +317,7 @@ def main():
         g.set_profiling(False)
         return max_over_ranks(statistics.mean(gens), dev), max_over_ranks(statistics.mean(jumps), dev)
 
-    gen_ms, jump_wait_ms = kernel_times()
-    g.set_prefetch(False)
-    step()
-    gen_iso_ms, jump_ms = kernel_times()
-    g.set_prefetch(True)
+    gen_ms, jump_ms = kernel_times()
 
     # -- global checksum of one full 2^34 range (config 4 verification)
     g.seek(start)
@@ -328,7 +368,6 @@ def main():
     peak, peak_src = measured_peak()
     bytes_per_launch = count * 4
     achieved = bytes_per_launch / (gen_ms * 1e-3) / 1e9
-    achieved_iso = bytes_per_launch / (gen_iso_ms * 1e-3) / 1e9
     traffic = profiled_traffic()
     line = {
         "metric": METRIC, "value": T / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -342,15 +381,13 @@ def main():
                    "parallelism": f"stream partition x{world} ({args.scaling})"},
         "gpu_launches": launches,
         "per_gpu_value": count / (ms * 1e-3),
-        "timing_breakdown_ms": {"gen_kernel_in_situ": gen_ms, "positioning_wait_in_situ": jump_wait_ms,
-                                "gen_kernel_isolated": gen_iso_ms, "positioning_jumps_isolated": jump_ms,
-                                "note": "in situ = as timed (next step's positioning prefetched on a side "
-                                        "stream, overlapping generation); isolated = prefetch off"},
+        "timing_breakdown_ms": {"gen_kernel": gen_ms, "positioning_jumps": jump_ms,
+                                "note": "CUDA events on the fill's stream around the chunk-positioning jump "
+                                        "launch and the generation launch of each step (back to back)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": (traffic or {}).get("dram_bytes_per_launch"),
-                     "kernel": "vmt_gen_kernel (in situ)", "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": bytes_per_launch,
-                     "achieved_isolated": achieved_iso, "frac_isolated": achieved_iso / peak},
+                     "kernel": "vmt_gen_kernel", "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": bytes_per_launch},
         "checksum_xor": f"0x{csum:08x}",
         "clocks": clk,
         "e2e": e2e,

@@ -128,7 +128,9 @@ int vmt_charpoly(uint64_t* out313);
 /* Kernel tuning for the generation path: chunks per fill (0 = auto), and
  * the CTA shape variant (0 = auto). Returns VMT_EINVAL for unknown variants. */
 int vmt_set_tuning(vmt_handle h, unsigned max_chunks, int variant);
-/* Steady-state positioning prefetch (default on): while a fill of >= 2^24
+/* Steady-state positioning prefetch (default off: with the generation kernel
+ * ALU-saturated the overlapped jumps slow it by as much as they save, see
+ * DESIGN.md section 5): while a fill of >= 2^24
  * words generates, the chunk start states of the predicted next fill (same
  * size, same gap) are computed on a side stream; a matching next fill skips
  * its positioning jumps. Results are identical either way. */

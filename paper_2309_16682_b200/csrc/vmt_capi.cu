@@ -427,7 +427,7 @@ struct vmt_generator {
 
     DevBuf<std::uint32_t> chunks;    // [C][624][L]
     DevBuf<std::uint32_t> chunks_alt; // prefetched chunk states of the predicted next fill
-    bool prefetch = true;            // position the predicted next fill while this one generates
+    bool prefetch = false;           // position the predicted next fill while this one generates
     bool pref_valid = false;
     std::uint64_t pref_b0 = 0, pref_B = 0, pref_C = 0;
     std::uint64_t last_end = ~0ull;  // end position of the previous GPU fill
@@ -571,10 +571,13 @@ void reposition(vmt_generator* h, std::uint64_t target, cudaStream_t st) {
 
 // Chunk count for a fill of n words: every chunk but the first costs L lane
 // jumps (positioning), every chunk adds generation parallelism. Minimise
-//   t(C) = t_jump((C-1) L) + n / min(peak, C * L * r_lane)
-// with constants measured on B200: a lane jump costs
-// 0.43 us of whole-GPU throughput with a latency floor of 0.16-0.5 ms, a
-// lane-state generates ~2.8e8 words/s, the store path saturates at ~1.4e12.
+//   t(C) = t_jump((C-1) L) + (n / C) / min(L * r_lane, peak_sm / k),
+// k = ceil(C / sms) chunks sharing the busiest SM, with constants measured on
+// B200: a lane jump costs 0.43 us of whole-GPU
+// throughput with a latency floor of 0.16-0.5 ms, one lane generates ~2.9e8
+// words/s, an SM's store path saturates at ~1.5e12 / 148 words/s. Past one
+// chunk per SM only whole waves (multiples of sms) are candidates: a partial
+// wave leaves the SMs with one chunk more as the tail.
 std::uint64_t plan_chunks(unsigned L, std::uint64_t n, std::uint64_t c_max, int sms) {
     const double per_jump = 0.43e-6 * 148.0 / (double)sms;
     auto t_jump = [&](double jobs) -> double {
@@ -583,24 +586,26 @@ std::uint64_t plan_chunks(unsigned L, std::uint64_t n, std::uint64_t c_max, int 
         const double floor_s = jobs <= sms * 4.0 ? 0.16e-3 : (jobs <= sms * 16.0 ? 0.37e-3 : 0.0);
         return std::max(floor_s, jobs * per_jump);
     };
-    const double r_lane = 2.8e8, peak = 1.4e12 * (double)sms / 148.0;
+    const double r_lane = 2.9e8, peak_sm = 1.5e12 / 148.0;
     auto t = [&](std::uint64_t C) {
-        return t_jump(double(C - 1) * L) + double(n) / std::min(peak, double(C) * L * r_lane);
+        const double k = (double)((C + sms - 1) / sms);
+        return t_jump(double(C - 1) * L) + (double(n) / double(C)) / std::min(L * r_lane, peak_sm / k);
     };
     std::uint64_t best = 1;
     double tb = t(1);
-    for (std::uint64_t C = 2; C <= c_max; C = (C * 5 + 3) / 4) { // ~25% steps
+    auto consider = [&](std::uint64_t C) {
         const double tc = t(C);
-        if (tc < tb) {
+        if (tc < tb * 0.97) { // a candidate must win clearly: fewer chunks is less positioning risk
             tb = tc;
             best = C;
         }
-    }
-    if (t(c_max) < tb)
-        best = c_max;
-    // whole waves of one chunk per SM are the sweet spot for large fills
-    if (best > (std::uint64_t)sms && best < c_max && t((std::uint64_t)sms) <= tb * 1.02)
-        best = (std::uint64_t)sms;
+    };
+    const std::uint64_t one_wave = std::min<std::uint64_t>(c_max, (std::uint64_t)sms);
+    for (std::uint64_t C = 2; C < one_wave; C = (C * 5 + 3) / 4) // ~25% steps
+        consider(C);
+    consider(one_wave);
+    for (std::uint64_t C = 2 * (std::uint64_t)sms; C <= c_max; C += (std::uint64_t)sms)
+        consider(C);
     return best;
 }
 
@@ -611,7 +616,6 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
         return;
     const std::uint64_t P0 = h->gpos, P1 = h->gpos + n;
     const std::uint64_t b0 = P0 / h->bw, b1 = (P1 + h->bw - 1) / h->bw;
-    reposition(h, b0, st);
     if (h->profile)
         VMT_CUDA(cudaEventRecord(h->ev[0], st));
     const Variant& v = pick_variant(h->L, h->variant);
@@ -647,9 +651,12 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     const bool use_pref = h->pref_valid && h->pref_b0 == b0 && h->pref_B == B && h->pref_C == C;
     h->pref_valid = false;
     if (use_pref) {
+        // chunk 0 is the prefetched state at b0, so cur needs no re-positioning
+        // (the generation kernel saves the next one)
         VMT_CUDA(cudaStreamWaitEvent(st, h->ev_pref, 0));
         h->chunks.swap(h->chunks_alt);
     } else {
+        reposition(h, b0, st);
         h->chunks.reserve((size_t)C * kN * h->L);
         VMT_CUDA(cudaMemcpyAsync(h->chunks.p, h->cur.p, (size_t)kN * h->L * 4, cudaMemcpyDeviceToDevice, st));
         if (C > 1) {

@@ -59,6 +59,10 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+#ifndef VMT_GEN_HIST
+#define VMT_GEN_HIST 1
+#endif
+
 template <int MODE>
 __host__ __device__ constexpr int elem_bytes() {
     return (MODE == MODE_F64 || MODE == MODE_F64_REAL3 || MODE == MODE_F64_RES53) ? 8 : 4;
@@ -195,18 +199,33 @@ struct StageCtl {
 // the run's first p; a: slot of x_{p+397}; wsl: slot receiving x_{p+624}.
 // All ring loads are issued before any ring store (the stores go to slots no
 // thread reads in this window), so the compiler is free to overlap them.
-template <int LT, int L, int R, int VW, int W, int MODE, bool VEC, bool FULL, bool STAGE>
+//
+// HIST: the run's x_p .. x_{p+R-1} are the words this same thread computed
+// three windows (one block) earlier, kept in registers (H) instead of being
+// re-read from the ring; only x_{p+R} (the next run's first word) and the
+// x_{p+397} operands come from shared memory.
+template <int LT, int L, int R, int VW, int W, int MODE, bool VEC, bool FULL, bool STAGE, bool HIST>
 __device__ __forceinline__ void gen_window(std::uint32_t* ring, int base, int a, int wsl, int q, int rho,
                                            unsigned long long g0, const GenParams& p, void* out,
-                                           std::uint32_t* acc, StageCtl& sc, int tid) {
+                                           std::uint32_t* acc, StageCtl& sc, int tid,
+                                           std::uint32_t (&H)[R][GenShape<L, R, VW, W>::V]) {
     using S = GenShape<L, R, VW, W>;
     constexpr int V = S::V;
     using VT = typename VecT<V>::T;
     using E = typename ElemT<MODE>::T;
     std::uint32_t X[R + 1][V], M[R][V];
+    if (HIST) {
 #pragma unroll
-    for (int i = 0; i <= R; ++i)
-        VecT<V>::get(*reinterpret_cast<const VT*>(ring + (base + i) * L + q * V), X[i]);
+        for (int i = 0; i < R; ++i)
+#pragma unroll
+            for (int v = 0; v < V; ++v)
+                X[i][v] = H[i][v];
+        VecT<V>::get(*reinterpret_cast<const VT*>(ring + (base + R) * L + q * V), X[R]);
+    } else {
+#pragma unroll
+        for (int i = 0; i <= R; ++i)
+            VecT<V>::get(*reinterpret_cast<const VT*>(ring + (base + i) * L + q * V), X[i]);
+    }
 #pragma unroll
     for (int i = 0; i < R; ++i)
         VecT<V>::get(*reinterpret_cast<const VT*>(ring + (a + i) * L + q * V), M[i]);
@@ -223,6 +242,11 @@ __device__ __forceinline__ void gen_window(std::uint32_t* ring, int base, int a,
         for (int v = 0; v < V; ++v)
             nw[v] = twist(X[i][v], X[i + 1][v], M[i][v]);
         *reinterpret_cast<VT*>(ring + (wsl + i) * L + q * V) = VecT<V>::make(nw);
+        if (HIST) {
+#pragma unroll
+            for (int v = 0; v < V; ++v)
+                H[i][v] = nw[v];
+        }
         if (MODE == MODE_XOR) {
             // temper is GF(2)-linear: XOR the untempered words, temper once
             // at the end (vmt_xor_reduce_kernel)
@@ -365,11 +389,20 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::NT, GenShape<L, R,
     constexpr unsigned long long ww = (unsigned long long)W * LT; // stream words per window (all lanes)
     const bool save_here = p.save_state != nullptr && (!batch || chunk == 0);
     int blk_base_slot = 0; // slot of x_{624 r} for the current block r (= 624 r mod RING)
-    for (unsigned long long blk = b_lo; blk < b_hi; ++blk) {
-        if (save_here && blk == p.save_block)
-            save_boundary<LT, L, S::RING>(ring, blk_base_slot, p.save_state, col0, tid, S::NT);
-#pragma unroll 1
-        for (int wi = 0; wi < kN / W; ++wi) {
+    constexpr int kWins = kN / W;
+    // (3 windows x R x V history registers: with V = 4 that spills)
+    constexpr bool kHist = VMT_GEN_HIST && kWins == 3 && V <= 2;
+    std::uint32_t H[kHist ? kWins : 1][R][V];
+    if (kHist) {
+        // the first block's x_p of each window of this run: the chunk state
+#pragma unroll
+        for (int wi = 0; wi < (kHist ? kWins : 1); ++wi)
+#pragma unroll
+            for (int i = 0; i < R; ++i)
+                VecT<V>::get(*reinterpret_cast<const VT*>(ring + (wi * W + rho * R + i) * L + q * V), H[wi][i]);
+    }
+    auto window = [&](unsigned long long blk, int wi, std::uint32_t (&Hw)[R][V]) {
+        {
             int wstart = blk_base_slot + wi * W;
             if (wstart >= S::RING)
                 wstart -= S::RING;
@@ -385,14 +418,14 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::NT, GenShape<L, R,
             const bool wfull = gw >= p.pos_begin && gw + ww <= p.pos_end;
             const bool staged = kStaged && tma_ok && wfull;
             if (staged)
-                gen_window<LT, L, R, VW, W, MODE, VEC, true, kStaged>(ring, base, a, wsl, q, rho, g0, p, out, acc,
-                                                                      sc, tid);
+                gen_window<LT, L, R, VW, W, MODE, VEC, true, kStaged, kHist>(ring, base, a, wsl, q, rho, g0, p, out,
+                                                                             acc, sc, tid, Hw);
             else if (wfull)
-                gen_window<LT, L, R, VW, W, MODE, VEC, true, false>(ring, base, a, wsl, q, rho, g0, p, out, acc, sc,
-                                                                    tid);
+                gen_window<LT, L, R, VW, W, MODE, VEC, true, false, kHist>(ring, base, a, wsl, q, rho, g0, p, out,
+                                                                           acc, sc, tid, Hw);
             else
-                gen_window<LT, L, R, VW, W, MODE, VEC, false, false>(ring, base, a, wsl, q, rho, g0, p, out, acc,
-                                                                     sc, tid);
+                gen_window<LT, L, R, VW, W, MODE, VEC, false, false, kHist>(ring, base, a, wsl, q, rho, g0, p, out,
+                                                                            acc, sc, tid, Hw);
             __syncthreads();
             if (kStaged) {
                 if (staged && tid == 0) {
@@ -406,6 +439,20 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::NT, GenShape<L, R,
                 if (staged)
                     sc.prev_staged = true; // a bulk copy of the buffer is outstanding
             }
+        }
+    };
+    for (unsigned long long blk = b_lo; blk < b_hi; ++blk) {
+        if (save_here && blk == p.save_block)
+            save_boundary<LT, L, S::RING>(ring, blk_base_slot, p.save_state, col0, tid, S::NT);
+        if (kHist) {
+            // fully unrolled so each window's history registers are static
+#pragma unroll
+            for (int wi = 0; wi < (kHist ? kWins : 1); ++wi)
+                window(blk, wi, H[wi]);
+        } else {
+#pragma unroll 1
+            for (int wi = 0; wi < kWins; ++wi)
+                window(blk, wi, H[0]);
         }
         blk_base_slot += kN;
         if (blk_base_slot >= S::RING)

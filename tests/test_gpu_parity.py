@@ -284,6 +284,7 @@ def test_prefetched_positioning_matches(oracle):
     plan = [(n, 0), (n, 0), (n, gap), (n, gap), (n - 7, 0), (n, 0)]
     pos = 0
     g = V.VmtEngine(L, 77, q)
+    g.set_prefetch(True)
     for i, (size, skip) in enumerate(plan):
         g.skip(skip)
         pos += skip
