@@ -125,6 +125,57 @@ int vmt_jump_poly(uint64_t d_lo, uint64_t d_hi, uint64_t* out312);
 int vmt_jump_poly_pow2(unsigned q, uint64_t* out312);
 int vmt_charpoly(uint64_t* out313);
 
+/* ---- GF(2) jump matrices (f2_matrix.hpp, jump_file.hpp) -------------------
+ * A matrix is 19937 rows x 312 little-endian u64 (F2Matrix row-major payload,
+ * f2_matrix.hpp:13-21 and 49-51; row i = image of basis vector i in the
+ * effective layout, mt19937.cpp:57-101). Row/vector buffers may be host or
+ * device memory. */
+#define VMT_MATRIX_DIM 19937u
+#define VMT_MATRIX_ROW_WORDS 312u
+#define VMT_MATRIX_WORDS (19937ull * 312ull)
+
+/* F^d for d = d_hi*2^64 + d_lo, computed on the GPU as 19937 polynomial jumps
+ * of the basis states. vmt_jump_matrix_pow2(q) equals the reference's
+ * mat_pow2(build_transition_matrix(), q) (f2_matrix.cpp:138-177,179-228)
+ * byte for byte, for every q including the full-period exponents. */
+int vmt_jump_matrix(uint64_t d_lo, uint64_t d_hi, uint64_t* rows, int device, void* stream);
+int vmt_jump_matrix_pow2(unsigned q, uint64_t* rows, int device, void* stream);
+
+/* write_jump_matrix_file / read_jump_matrix_file (jump_file.hpp:37,
+ * jump_file.cpp:117-137): the 20-byte "VMTJ" header (version 1, dimension,
+ * exponent, reserved 0) plus the payload, written through a temporary file.
+ * The reader applies the reference's checks (magic, version, reserved,
+ * zero dimension, payload size, padding bits -> VMT_EIO); a well-formed file
+ * of another dimension is VMT_EINVAL. rows == NULL validates without
+ * reading the payload. */
+int vmt_write_jump_matrix_file(const char* path, const uint64_t* rows, unsigned exponent);
+int vmt_read_jump_matrix_file(const char* path, uint64_t* rows, unsigned* exponent);
+
+/* compute_jump_matrix (jump_file.cpp:171-209; the CLI `jump` command): writes
+ * the file for F^(2^exponent) -- milliseconds on the GPU instead of
+ * `exponent` CPU squarings (~50 h at the full period). */
+int vmt_compute_jump_matrix_file(const char* path, unsigned exponent, int device);
+
+/* vec_mat_mul (f2_matrix.cpp:119-136) for n effective vectors (n x 312 u64):
+ * out_i = vecs_i * M, the XOR of the rows at the set bits of vecs_i. */
+int vmt_vec_mat_mul(const uint64_t* vecs, uint64_t n, const uint64_t* rows, uint64_t* out, int device,
+                    void* stream);
+
+/* jump_state (jump.cpp:27-33) with a caller matrix, for n boundary states
+ * (n x 624 words): dst_i = effective_to_state(state_to_effective(src_i) * M);
+ * the dead low bits of word 0 come out zero (mt19937.cpp:79). */
+int vmt_jump_states_matrix(const uint32_t* src, uint64_t n, const uint64_t* rows, uint32_t* dst, int device,
+                           void* stream);
+
+/* VmtEngine<M>(seed, jump_matrix, jump_exponent) (engine.hpp:54-63) with the
+ * matrix de-phasing of make_dephased_states (jump.cpp:35-53): lane t = lane
+ * t-1 * B on the GPU. rows may be NULL for lanes == 1 (engine.hpp:66-68).
+ * vmt_create_from_file reads a .vmtj file and adopts its exponent (the CLI's
+ * resolve_jump with an explicit file, vmt19937_main.cpp:30-37). */
+int vmt_create_from_matrix(uint32_t seed, unsigned lanes, const uint64_t* rows, unsigned exponent, int device,
+                           vmt_handle* out);
+int vmt_create_from_file(uint32_t seed, unsigned lanes, const char* path, int device, vmt_handle* out);
+
 /* Kernel tuning for the generation path: chunks per fill (0 = auto), and
  * the CTA shape variant (0 = auto). Returns VMT_EINVAL for unknown variants. */
 int vmt_set_tuning(vmt_handle h, unsigned max_chunks, int variant);

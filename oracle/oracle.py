@@ -202,6 +202,10 @@ class RefLib:
         lib.vref_simd_backend.argtypes = [c.c_uint]
         lib.vref_jump_by.argtypes = [_u32p, c.c_uint64, _u32p]
         lib.vref_mt64.argtypes = [c.c_uint64, c.c_uint64, _u64p]
+        lib.vref_write_pow2_matrix_file.argtypes = [c.c_uint, c.c_char_p]
+        lib.vref_read_jump_matrix_file.argtypes = [c.c_char_p, c.c_void_p, c.POINTER(c.c_uint),
+                                                   c.POINTER(c.c_uint)]
+        lib.vref_dephased_states_file.argtypes = [c.c_uint32, c.c_uint, c.c_char_p, _u32p]
         self.lib = lib
 
     @staticmethod
@@ -248,6 +252,29 @@ class RefLib:
         out = np.empty(count, np.uint64)
         self.lib.vref_mt64(seed, count, out)
         return out
+
+    def write_pow2_matrix_file(self, q, path):
+        """write_jump_matrix_file(path, F^(2^q), q) -- compute_jump_matrix's bytes."""
+        self._ok(self.lib.vref_write_pow2_matrix_file(q, os.fsencode(path)), "write_jump_matrix_file")
+
+    def read_jump_matrix_file(self, path, rows=True):
+        """read_jump_matrix_file: (rows (dim, ceil(dim/64)) uint64 or None, exponent); raises
+        RuntimeError(rc) on the reference's exceptions (-1 invalid_argument, -3 runtime_error)."""
+        dim, e = ctypes.c_uint(), ctypes.c_uint()
+        rc = self.lib.vref_read_jump_matrix_file(os.fsencode(path), None, ctypes.byref(dim), ctypes.byref(e))
+        if rc != 0:
+            raise RuntimeError(f"reference read_jump_matrix_file failed rc={rc}")
+        if not rows:
+            return None, e.value
+        out = np.empty((dim.value, (dim.value + 63) // 64), np.uint64)
+        self._ok(self.lib.vref_read_jump_matrix_file(os.fsencode(path), out.ctypes.data, None, None),
+                 "read_jump_matrix_file")
+        return out, e.value
+
+    def dephased_states_file(self, seed, lanes, path):
+        out = np.empty(624 * lanes, np.uint32)
+        self._ok(self.lib.vref_dephased_states_file(seed, lanes, os.fsencode(path), out), "dephased_states_file")
+        return out.reshape(lanes, 624)
 
     def run_benchmark(self, lanes, mode, count, seed, q):
         s = ctypes.c_double()

@@ -11,6 +11,7 @@
 //   jump_state              proj/src/jump.cpp:27-33
 //   mat_mul / transition F  proj/src/f2_matrix.cpp:138-228
 //   run_benchmark           proj/src/bench.cpp:99-120
+//   .vmtj files             proj/src/jump_file.cpp:117-209
 // Error mapping: invalid_argument -> -1, logic_error -> -2, other -> -3.
 
 #include <atomic>
@@ -27,6 +28,7 @@
 #include "vmt19937/bench.hpp"
 #include "vmt19937/engine.hpp"
 #include "vmt19937/jump.hpp"
+#include "vmt19937/jump_file.hpp"
 #include "vmt19937/lane_ops.hpp"
 
 using namespace vmt19937;
@@ -297,6 +299,36 @@ int vref_jump_by(const std::uint32_t* in, std::uint64_t d, std::uint32_t* out) {
             if ((d >> i) & 1u)
                 s = jump_state(s, transition_power(i));
         std::memcpy(out, s.words().data(), 624 * 4);
+    });
+}
+
+// write_jump_matrix_file(path, F^(2^q), q) with the cached ladder rung --
+// the bytes compute_jump_matrix (jump_file.cpp:171-209) writes for exponent q.
+int vref_write_pow2_matrix_file(unsigned q, const char* path) {
+    return guarded([&] { write_jump_matrix_file(path, transition_power(q), q); });
+}
+
+// read_jump_matrix_file (jump_file.cpp:125-137): rows (nullable) and exponent.
+int vref_read_jump_matrix_file(const char* path, std::uint64_t* rows, unsigned* dim, unsigned* exponent) {
+    return guarded([&] {
+        LoadedJumpMatrix m = read_jump_matrix_file(path);
+        if (dim)
+            *dim = unsigned(m.matrix.dim());
+        if (exponent)
+            *exponent = m.exponent;
+        if (rows)
+            std::memcpy(rows, m.matrix.data().data(), m.matrix.data().size() * 8);
+    });
+}
+
+// make_dephased_states(Mt19937(seed), JumpSpec{exponent, lanes}, B) with B
+// read from a .vmtj file.
+int vref_dephased_states_file(std::uint32_t seed, unsigned lanes, const char* path, std::uint32_t* out) {
+    return guarded([&] {
+        LoadedJumpMatrix m = read_jump_matrix_file(path);
+        auto st = make_dephased_states(Mt19937(seed), JumpSpec{m.exponent, lanes}, m.matrix);
+        for (unsigned t = 0; t < lanes; ++t)
+            std::memcpy(out + std::size_t(t) * 624, st[t].words().data(), 624 * 4);
     });
 }
 

@@ -31,11 +31,16 @@ __all__ = [
     "JumpSpec", "QueryMode", "VmtConfig", "VmtGenerator", "VmtEngine", "batch_fill_u32",
     "jump_states", "seed_states", "charpoly", "jump_poly", "jump_poly_pow2", "VmtError",
     "InvalidArgument", "LogicError", "VMT_F32_24", "VMT_F64_32", "VMT_F64_REAL3", "VMT_F64_RES53",
-    "KEFFECTIVE_BITS", "KSTATE_LEN",
+    "KEFFECTIVE_BITS", "KSTATE_LEN", "MATRIX_DIM", "MATRIX_ROW_WORDS", "jump_matrix", "jump_matrix_pow2",
+    "write_jump_matrix_file", "read_jump_matrix_file", "compute_jump_matrix", "jump_matrix_file_name",
+    "vec_mat_mul", "jump_state_matrix",
 ]
 
 KSTATE_LEN = 624
 KEFFECTIVE_BITS = 19937
+MATRIX_DIM = 19937
+MATRIX_ROW_WORDS = 312
+MATRIX_WORDS = MATRIX_DIM * MATRIX_ROW_WORDS
 
 
 class QueryMode(enum.IntEnum):
@@ -127,9 +132,29 @@ def _check_dtype(buf, np_dtype, torch_name: str) -> None:
 class VmtGenerator:
     """Runtime-lane-count VMT19937 generator on one GPU (engine.hpp:160-207)."""
 
-    def __init__(self, seed: int, cfg: Optional[VmtConfig] = None, device: int = 0, *, lane_states=None):
+    def __init__(self, seed: int, cfg: Optional[VmtConfig] = None, device: int = 0, *, lane_states=None,
+                 jump_matrix=None, jump_matrix_file: Optional[str] = None):
+        """``jump_matrix`` (19937 x 312 uint64 rows, host or device) or
+        ``jump_matrix_file`` (.vmtj) de-phase with a GF(2) matrix like the
+        reference's VmtGenerator(seed, cfg, F2Matrix) (engine.hpp:162-167); the
+        file's exponent is adopted. Otherwise the polynomial jump is used."""
         self._h = ctypes.c_void_p()
-        if lane_states is not None:
+        if jump_matrix_file is not None:
+            cfg = cfg or VmtConfig(1)
+            cfg.validate()
+            check(lib.vmt_create_from_file(seed & 0xFFFFFFFF, cfg.lanes, str(jump_matrix_file).encode(), device,
+                                           ctypes.byref(self._h)))
+            self.cfg = VmtConfig(cfg.lanes, cfg.mode, int(lib.vmt_jump_exponent(self._h)))
+        elif jump_matrix is not None:
+            cfg = cfg or VmtConfig(1)
+            cfg.validate()
+            addr, keep, n, _ = _ptr(jump_matrix)
+            if n != MATRIX_WORDS:
+                raise InvalidArgument(_capi.VMT_EINVAL, f"jump matrix must have {MATRIX_WORDS} uint64 words")
+            check(lib.vmt_create_from_matrix(seed & 0xFFFFFFFF, cfg.lanes, addr, cfg.jump_exponent, device,
+                                             ctypes.byref(self._h)))
+            self.cfg = cfg
+        elif lane_states is not None:
             arr = np.ascontiguousarray(lane_states, dtype=np.uint32)
             lanes = arr.size // KSTATE_LEN
             check(lib.vmt_create_from_states(arr.ctypes.data, lanes, device, ctypes.byref(self._h)))
@@ -317,4 +342,83 @@ def jump_poly(d: int) -> np.ndarray:
 def jump_poly_pow2(q: int) -> np.ndarray:
     out = np.empty(312, np.uint64)
     check(lib.vmt_jump_poly_pow2(q, out.ctypes.data))
+    return out
+
+
+# ---- GF(2) jump matrices (f2_matrix.hpp, jump_file.hpp) ----------------------
+def _matrix_out(out, device: int):
+    if out is None:
+        return np.empty((MATRIX_DIM, MATRIX_ROW_WORDS), np.uint64)
+    _check_dtype(out, np.uint64, "uint64")
+    if _ptr(out)[2] != MATRIX_WORDS:
+        raise InvalidArgument(_capi.VMT_EINVAL, f"matrix buffer must have {MATRIX_WORDS} words")
+    return out
+
+
+def jump_matrix(d: int, out=None, device: int = 0, stream=None):
+    """F^d (19937 x 312 uint64 rows; numpy by default, or a given numpy/torch
+    buffer), computed on the GPU as 19937 polynomial jumps of basis states."""
+    out = _matrix_out(out, device)
+    addr, keep, _, kind = _ptr(out)
+    check(lib.vmt_jump_matrix(d & (2**64 - 1), d >> 64, addr, device, _stream_for(kind, stream)))
+    return out
+
+
+def jump_matrix_pow2(q: int, out=None, device: int = 0, stream=None):
+    """F^(2^q) == mat_pow2(build_transition_matrix(), q) (f2_matrix.cpp:138-228)."""
+    out = _matrix_out(out, device)
+    addr, keep, _, kind = _ptr(out)
+    check(lib.vmt_jump_matrix_pow2(q, addr, device, _stream_for(kind, stream)))
+    return out
+
+
+def jump_matrix_file_name(exponent: int) -> str:
+    """jump_file.cpp:167-169."""
+    return f"F_2p{exponent}.vmtj"
+
+
+def write_jump_matrix_file(path: str, rows, exponent: int) -> None:
+    """write_jump_matrix_file (jump_file.cpp:117-123)."""
+    addr, keep, n, _ = _ptr(rows)
+    if n != MATRIX_WORDS:
+        raise InvalidArgument(_capi.VMT_EINVAL, f"matrix must have {MATRIX_WORDS} uint64 words")
+    check(lib.vmt_write_jump_matrix_file(str(path).encode(), addr, exponent))
+
+
+def read_jump_matrix_file(path: str, rows: bool = True):
+    """read_jump_matrix_file (jump_file.cpp:125-137): (rows or None, exponent).
+    Format errors raise VmtError(VMT_EIO) like the reference's runtime_error."""
+    e = ctypes.c_uint()
+    if not rows:
+        check(lib.vmt_read_jump_matrix_file(str(path).encode(), None, ctypes.byref(e)))
+        return None, e.value
+    out = np.empty((MATRIX_DIM, MATRIX_ROW_WORDS), np.uint64)
+    check(lib.vmt_read_jump_matrix_file(str(path).encode(), out.ctypes.data, ctypes.byref(e)))
+    return out, e.value
+
+
+def compute_jump_matrix(exponent: int, out: str, device: int = 0) -> None:
+    """compute_jump_matrix (jump_file.cpp:171-209): writes F^(2^exponent) to `out`."""
+    check(lib.vmt_compute_jump_matrix_file(str(out).encode(), exponent, device))
+
+
+def vec_mat_mul(vecs, rows, device: int = 0):
+    """vec_mat_mul (f2_matrix.cpp:119-136) for n x 312 uint64 effective vectors."""
+    v = np.ascontiguousarray(vecs, np.uint64).reshape(-1, MATRIX_ROW_WORDS)
+    out = np.empty_like(v)
+    addr, keep, n, _ = _ptr(rows)
+    if n != MATRIX_WORDS:
+        raise InvalidArgument(_capi.VMT_EINVAL, f"matrix must have {MATRIX_WORDS} uint64 words")
+    check(lib.vmt_vec_mat_mul(v.ctypes.data, v.shape[0], addr, out.ctypes.data, device, None))
+    return out
+
+
+def jump_state_matrix(states, rows, device: int = 0):
+    """jump_state (jump.cpp:27-33) with a caller matrix, n x 624 boundary states."""
+    s = np.ascontiguousarray(states, np.uint32).reshape(-1, KSTATE_LEN)
+    out = np.empty_like(s)
+    addr, keep, n, _ = _ptr(rows)
+    if n != MATRIX_WORDS:
+        raise InvalidArgument(_capi.VMT_EINVAL, f"matrix must have {MATRIX_WORDS} uint64 words")
+    check(lib.vmt_jump_states_matrix(s.ctypes.data, s.shape[0], addr, out.ctypes.data, device, None))
     return out

@@ -24,6 +24,9 @@ EXPORTS = [
     "vmt_skip", "vmt_seek", "vmt_synchronize", "vmt_export_state", "vmt_batch_fill_u32", "vmt_jump_states", "vmt_seed_states",
     "vmt_jump_poly", "vmt_jump_poly_pow2", "vmt_charpoly", "vmt_set_tuning", "vmt_set_prefetch", "vmt_set_profiling", "vmt_last_timings", "vmt_stats",
     "vmt_status_string", "vmt_last_error", "vmt_version",
+    "vmt_jump_matrix", "vmt_jump_matrix_pow2", "vmt_write_jump_matrix_file", "vmt_read_jump_matrix_file",
+    "vmt_compute_jump_matrix_file", "vmt_vec_mat_mul", "vmt_jump_states_matrix", "vmt_create_from_matrix",
+    "vmt_create_from_file",
 ]
 
 
@@ -85,6 +88,16 @@ def _load() -> ctypes.CDLL:
         "vmt_status_string": (c.c_char_p, [c.c_int]),
         "vmt_last_error": (c.c_char_p, []),
         "vmt_version": (c.c_int, []),
+        "vmt_jump_matrix": (c.c_int, [c.c_uint64, c.c_uint64, c.c_void_p, c.c_int, c.c_void_p]),
+        "vmt_jump_matrix_pow2": (c.c_int, [c.c_uint, c.c_void_p, c.c_int, c.c_void_p]),
+        "vmt_write_jump_matrix_file": (c.c_int, [c.c_char_p, c.c_void_p, c.c_uint]),
+        "vmt_read_jump_matrix_file": (c.c_int, [c.c_char_p, c.c_void_p, c.POINTER(c.c_uint)]),
+        "vmt_compute_jump_matrix_file": (c.c_int, [c.c_char_p, c.c_uint, c.c_int]),
+        "vmt_vec_mat_mul": (c.c_int, [c.c_void_p, c.c_uint64, c.c_void_p, c.c_void_p, c.c_int, c.c_void_p]),
+        "vmt_jump_states_matrix": (c.c_int, [c.c_void_p, c.c_uint64, c.c_void_p, c.c_void_p, c.c_int,
+                                             c.c_void_p]),
+        "vmt_create_from_matrix": (c.c_int, [c.c_uint32, c.c_uint, c.c_void_p, c.c_uint, c.c_int, c.POINTER(H)]),
+        "vmt_create_from_file": (c.c_int, [c.c_uint32, c.c_uint, c.c_char_p, c.c_int, c.POINTER(H)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -17,7 +17,6 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libvmt19937_b200.so")
 SOURCES = ["vmt_capi.cu", "gf2poly.cpp"]
-HEADERS = ["vmt_kernels.cuh", "vmt_common.cuh", "vmt_gen.cuh", "vmt_jump.cuh", "gf2poly.hpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -30,8 +29,9 @@ def _nvcc() -> str:
 
 def _fingerprint() -> str:
     h = hashlib.sha256()
-    for f in SOURCES + HEADERS:
+    for f in sorted(os.listdir(CSRC)):  # every source and header
         with open(os.path.join(CSRC, f), "rb") as fh:
+            h.update(f.encode())
             h.update(fh.read())
     with open(os.path.join(ROOT, "include", "vmt19937_b200.h"), "rb") as fh:
         h.update(fh.read())

@@ -1358,3 +1358,6 @@ const char* vmt_last_error(void) { return g_last_error.c_str(); }
 int vmt_version(void) { return 100; }
 
 } // extern "C"
+
+// GF(2) jump-matrix path: .vmtj files, vec_mat_mul, matrix de-phasing.
+#include "capi_matrix.inl"

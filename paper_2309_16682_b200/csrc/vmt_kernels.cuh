@@ -2,8 +2,10 @@
 //   vmt_common.cuh  constants, parameters, twist/temper arithmetic, conversions
 //   vmt_gen.cuh     vmt_gen_kernel: twist + temper + emit (the hot path)
 //   vmt_jump.cuh    vmt_jump_kernel (polynomial jump-ahead), seeding, reduction
+//   vmt_matrix.cuh  GF(2) jump matrices: basis states, effective layout, vec_mat_mul
 #pragma once
 
 #include "vmt_common.cuh"
 #include "vmt_gen.cuh"
 #include "vmt_jump.cuh"
+#include "vmt_matrix.cuh"

@@ -1,0 +1,143 @@
+// sm_100a kernels for the GF(2) jump-matrix path.
+//
+// The reference de-phases lanes with a dense 19937 x 19937 bit matrix
+// B = F^(2^q) (f2_matrix.hpp:13-21, jump.cpp:27-53) that it builds by q
+// successive squarings (mat_pow2, f2_matrix.cpp:138-177; ~50 h at the full
+// period) and stores as a .vmtj file (jump_file.hpp:12-22). Here:
+//
+//   * row i of F^d is the effective state of the basis state e_i jumped by d
+//     steps, so the whole matrix is 19937 independent polynomial jumps
+//     (vmt_jump_kernel on vmt_basis_kernel's states, then
+//     vmt_words_to_eff_kernel) -- milliseconds for any d, byte-identical to
+//     the reference's squaring ladder;
+//   * vec_mat_mul (f2_matrix.cpp:119-136: XOR of the rows at the set bits of
+//     v) runs as vmt_vec_mat_kernel, used to de-phase with a caller-supplied
+//     matrix exactly like make_dephased_states.
+//
+// Effective layout (mt19937.cpp:57-101): bit 0 = bit 31 of word 0, bits
+// 1..19936 = words 1..623 LSB first, packed into 312 little-endian u64 (624
+// u32 halves, the last 31 bits zero). As a 32-bit funnel:
+//   e32[h] = (W[h] >> 31) | (W[h+1] << 1)         h = 0..623, W[624] = 0
+//   W[0] = (e32[0] & 1) << 31,  W[k] = (e32[k-1] >> 1) | (e32[k] << 31)
+#pragma once
+
+#include <cstdint>
+
+#include "vmt_common.cuh"
+
+namespace vmt_b200 {
+
+constexpr int kDim = 19937;    // effective bits
+constexpr int kRowWords = 312; // u64 per row / vector
+constexpr int kRowHalves = 624;
+
+// Basis states e_{row0 + j}, j < n, as [n][624] words (buffer pre-zeroed).
+__global__ void vmt_basis_kernel(std::uint32_t* dst, int row0, int n) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n)
+        return;
+    const int row = row0 + j;
+    std::uint32_t* d = dst + (long long)j * kN;
+    if (row == 0)
+        d[0] = kUpperMask;
+    else
+        d[1 + (row - 1) / 32] = 1u << ((row - 1) % 32);
+}
+
+// words -> effective: state s word k at src + s*state_stride + k*word_stride,
+// effective halves to dst + s*624 (u32 view of the 312 u64).
+__global__ void vmt_words_to_eff_kernel(const std::uint32_t* src, long long state_stride, int word_stride,
+                                        std::uint32_t* dst, int n) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)n * kRowHalves)
+        return;
+    const long long s = i / kRowHalves;
+    const int h = (int)(i % kRowHalves);
+    const std::uint32_t* w = src + s * state_stride;
+    const std::uint32_t lo = w[(long long)h * word_stride];
+    const std::uint32_t hi = h + 1 < kN ? w[(long long)(h + 1) * word_stride] : 0u;
+    dst[i] = (lo >> 31) | (hi << 1);
+}
+
+// effective -> words (effective_to_words: the dead low bits of word 0 are zero).
+__global__ void vmt_eff_to_words_kernel(const std::uint32_t* src, std::uint32_t* dst, long long state_stride,
+                                        int word_stride, int n) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)n * kN)
+        return;
+    const long long s = i / kN;
+    const int k = (int)(i % kN);
+    const std::uint32_t* e = src + s * kRowHalves;
+    const std::uint32_t w = k == 0 ? (e[0] & 1u) << 31 : (e[k - 1] >> 1) | (e[k] << 31);
+    dst[s * state_stride + (long long)k * word_stride] = w;
+}
+
+// out[s] = v[s] * M for S vectors per CTA: CTA (cg, sb) owns the 32-byte
+// column group cg (4 u64, one DRAM sector) of vectors sb*S .. sb*S+S-1. Each
+// thread XORs the selected rows i = tid (mod 256) into its accumulators and
+// the CTA reduces them. Rows are read once per S vectors.
+constexpr int kVmS = 4;
+constexpr int kVmThreads = 256;
+constexpr int kVmGroups = kRowWords / 4; // 78
+
+__global__ void __launch_bounds__(kVmThreads) vmt_vec_mat_kernel(const std::uint64_t* __restrict__ vecs,
+                                                                   const std::uint64_t* __restrict__ mat,
+                                                                   std::uint64_t* __restrict__ out, int n) {
+    __shared__ std::uint64_t vs[kVmS][kRowWords];
+    __shared__ ulonglong4 red[kVmThreads / 32][kVmS];
+    const int cg = blockIdx.x, s0 = blockIdx.y * kVmS;
+    const int ns = n - s0 < kVmS ? n - s0 : kVmS;
+    for (int i = threadIdx.x; i < kVmS * kRowWords; i += kVmThreads) {
+        const int s = i / kRowWords, w = i % kRowWords;
+        vs[s][w] = s < ns ? vecs[(long long)(s0 + s) * kRowWords + w] : 0ull;
+    }
+    __syncthreads();
+    std::uint64_t acc[kVmS][4];
+#pragma unroll
+    for (int s = 0; s < kVmS; ++s)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            acc[s][c] = 0;
+    for (int i = threadIdx.x; i < kDim; i += kVmThreads) {
+        unsigned sel = 0;
+#pragma unroll
+        for (int s = 0; s < kVmS; ++s)
+            sel |= (unsigned)((vs[s][i >> 6] >> (i & 63)) & 1ull) << s;
+        if (sel == 0)
+            continue;
+        const ulonglong4 r = *reinterpret_cast<const ulonglong4*>(mat + (long long)i * kRowWords + cg * 4);
+#pragma unroll
+        for (int s = 0; s < kVmS; ++s)
+            if ((sel >> s) & 1u) {
+                acc[s][0] ^= r.x;
+                acc[s][1] ^= r.y;
+                acc[s][2] ^= r.z;
+                acc[s][3] ^= r.w;
+            }
+    }
+#pragma unroll
+    for (int s = 0; s < kVmS; ++s)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+                acc[s][c] ^= __shfl_xor_sync(0xFFFFFFFFu, acc[s][c], o);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0)
+#pragma unroll
+        for (int s = 0; s < kVmS; ++s)
+            red[warp][s] = make_ulonglong4(acc[s][0], acc[s][1], acc[s][2], acc[s][3]);
+    __syncthreads();
+    if (threadIdx.x < ns * 4) {
+        const int s = threadIdx.x / 4, c = threadIdx.x % 4;
+        std::uint64_t v = 0;
+#pragma unroll
+        for (int w = 0; w < kVmThreads / 32; ++w) {
+            const ulonglong4 t = red[w][s];
+            v ^= c == 0 ? t.x : c == 1 ? t.y : c == 2 ? t.z : t.w;
+        }
+        out[(long long)(s0 + s) * kRowWords + cg * 4 + c] = v;
+    }
+}
+
+} // namespace vmt_b200

@@ -11,7 +11,8 @@ Sources:
   polynomials x^(2^q) mod P, q = 19932..19936, by plain repeated squaring
   (with the period check x^(2^19937) == x).
 
-Usage: python tests/golden/make_golden.py [--skip-ladder]
+Usage: python tests/golden/make_golden.py [--skip-ladder] [--only vmtj]
+(--only SECTION recomputes one section into the existing golden.json)
 """
 from __future__ import annotations
 
@@ -40,8 +41,42 @@ def interleave_lane_outputs(lane_out: np.ndarray) -> np.ndarray:
     return lane_out.T.reshape(-1)
 
 
+VMTJ_EXPONENTS = (0, 1, 2, 5, 10, 16, 20, 24)
+
+
+def vmtj_section(r: RefLib, out: dict) -> None:
+    """SHA-256 of the .vmtj files the reference writes for F^(2^q)
+    (write_jump_matrix_file over mat_pow2, jump_file.cpp:117-123 -- the bytes
+    of its `jump` command), and the header fields."""
+    import tempfile
+    t0 = time.time()
+    files = {}
+    with tempfile.TemporaryDirectory() as d:
+        for q in VMTJ_EXPONENTS:
+            path = os.path.join(d, f"F_2p{q}.vmtj")
+            r.write_pow2_matrix_file(q, path)
+            with open(path, "rb") as f:
+                data = f.read()
+            rows = np.frombuffer(data, np.uint64, offset=20).reshape(19937, 312)
+            files[str(q)] = {"sha256": hashlib.sha256(data).hexdigest(), "size": len(data),
+                             "header_hex": data[:20].hex(),
+                             "row_xor_fold": int(np.bitwise_xor.reduce(rows, axis=None)),
+                             "row0": [int(v) for v in rows[0, :4]], "row19936": [int(v) for v in rows[-1, -4:]]}
+            print(f"vmtj q={q} {time.time() - t0:.1f}s", flush=True)
+    out["vmtj"] = files
+
+
 def main() -> None:
     skip_ladder = "--skip-ladder" in sys.argv
+    if "--only" in sys.argv:
+        section = sys.argv[sys.argv.index("--only") + 1]
+        path = os.path.join(HERE, "golden.json")
+        with open(path) as f:
+            out = json.load(f)
+        {"vmtj": vmtj_section}[section](RefLib(), out)
+        with open(path, "w") as f:
+            json.dump(out, f, indent=1)
+        return
     o, r = Oracle(), RefLib()
     out: dict = {}
     t0 = time.time()
@@ -115,6 +150,7 @@ def main() -> None:
     np.savez_compressed(os.path.join(HERE, "xpow2_full.npz"), **polys)
     out["period_check"] = "x^(2^19937) == x mod P"
     print(f"full-period polys {time.time() - t0:.1f}s", flush=True)
+    vmtj_section(r, out)
 
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(out, f, indent=1)
