@@ -198,6 +198,29 @@ int vmt_last_timings(vmt_handle h, float* jump_ms, float* gen_ms);
 int vmt_stats(vmt_handle h, uint64_t* gen_launches, uint64_t* jump_launches, uint64_t* other_launches,
               uint64_t* lane_jumps);
 
+/* ---- fused statistics consumer (stats.hpp, stats.cpp) ---------------------
+ * StatReport (stats.hpp:13-20). */
+typedef struct {
+    const char* name; /* static string */
+    uint64_t samples;
+    double statistic;
+    double p_value;
+    int pass;
+} vmt_stat_report;
+
+/* Consumes the next n words of the stream (like a fill, nothing stored: the
+ * generation kernel counts in shared memory): out257[0] = one bits,
+ * out257[1 + b] = occurrences of byte value b over the 4 bytes of each word. */
+int vmt_stat_counts(vmt_handle h, uint64_t n, uint64_t* out257, void* stream);
+/* monobit (stats.cpp:65-81) and chi2_bytes (stats.cpp:83-107) over the next
+ * `count` words, the counts from vmt_stat_counts and the statistic, p-value
+ * and pass flag by the reference's formulas. Undersized samples are
+ * VMT_EINVAL like the reference's std::invalid_argument. */
+int vmt_monobit(vmt_handle h, uint64_t count, vmt_stat_report* out);
+int vmt_chi2_bytes(vmt_handle h, uint64_t count, vmt_stat_report* out);
+/* detail::regularized_gamma_q (stats.hpp:47-50, stats.cpp:52-60). */
+int vmt_regularized_gamma_q(double a, double x, double* out);
+
 const char* vmt_status_string(int status);
 /* Message of the last failure on this thread. */
 const char* vmt_last_error(void);

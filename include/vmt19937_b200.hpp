@@ -1,8 +1,9 @@
 // vmt19937_b200.hpp -- C++ mirror of the reference's generator interface
 // (proj/include/vmt19937/engine.hpp, jump.hpp) over the C ABI in
 // vmt19937_b200.h. Reference code written against VmtEngine / VmtGenerator /
-// JumpSpec compiles against this header with the matrix arguments dropped:
-// de-phasing uses the jump polynomial on the GPU instead of a jump matrix.
+// JumpSpec / F2Matrix / the .vmtj functions compiles against this header:
+// the matrix constructors de-phase with the caller's matrix on the GPU
+// (make_dephased_states), the matrix-free ones with the jump polynomial.
 //
 // Errors are rethrown as the reference's exception classes:
 //   VMT_EINVAL -> std::invalid_argument, VMT_ESTATE -> std::logic_error,
@@ -66,6 +67,62 @@ struct VmtConfig {
     }
 };
 
+// Dense 19937 x 19937 GF(2) matrix (f2_matrix.hpp:13-61), row-major payload
+// of 312 u64 per row -- the .vmtj layout. Only the MT19937 dimension.
+class F2Matrix {
+public:
+    F2Matrix() = default;
+    static F2Matrix zeros() {
+        F2Matrix m;
+        m.words_.assign(VMT_MATRIX_WORDS, 0);
+        return m;
+    }
+    std::size_t dim() const { return words_.empty() ? 0 : VMT_MATRIX_DIM; }
+    std::size_t row_words() const { return VMT_MATRIX_ROW_WORDS; }
+    const std::uint64_t* row(std::size_t i) const { return words_.data() + i * VMT_MATRIX_ROW_WORDS; }
+    bool get(std::size_t r, std::size_t c) const { return (row(r)[c >> 6] >> (c & 63)) & 1u; }
+    const std::vector<std::uint64_t>& data() const { return words_; }
+    std::vector<std::uint64_t>& data() { return words_; }
+    friend bool operator==(const F2Matrix& a, const F2Matrix& b) { return a.words_ == b.words_; }
+
+private:
+    std::vector<std::uint64_t> words_;
+};
+
+// F^(2^q) == mat_pow2(build_transition_matrix(), q) (f2_matrix.cpp:138-228),
+// computed on the GPU.
+inline F2Matrix jump_matrix_pow2(unsigned q, int device = 0) {
+    F2Matrix m = F2Matrix::zeros();
+    check(vmt_jump_matrix_pow2(q, m.data().data(), device, nullptr));
+    return m;
+}
+// F^d for any 64-bit d.
+inline F2Matrix jump_matrix(std::uint64_t d, int device = 0) {
+    F2Matrix m = F2Matrix::zeros();
+    check(vmt_jump_matrix(d, 0, m.data().data(), device, nullptr));
+    return m;
+}
+
+// jump_file.hpp:26-45
+struct LoadedJumpMatrix {
+    F2Matrix matrix;
+    unsigned exponent;
+};
+inline void write_jump_matrix_file(const std::string& path, const F2Matrix& m, unsigned exponent) {
+    check(vmt_write_jump_matrix_file(path.c_str(), m.data().data(), exponent));
+}
+inline LoadedJumpMatrix read_jump_matrix_file(const std::string& path) {
+    LoadedJumpMatrix out{F2Matrix::zeros(), 0};
+    check(vmt_read_jump_matrix_file(path.c_str(), out.matrix.data().data(), &out.exponent));
+    return out;
+}
+inline std::string jump_matrix_file_name(unsigned exponent) { return "F_2p" + std::to_string(exponent) + ".vmtj"; }
+// compute_jump_matrix (jump_file.cpp:171-209) without checkpoints: the GPU
+// needs milliseconds, not hours.
+inline void compute_jump_matrix(unsigned exponent, const std::string& out, int device = 0) {
+    check(vmt_compute_jump_matrix_file(out.c_str(), exponent, device));
+}
+
 // Runtime-lane-count generator (engine.hpp:160-207). One owner per
 // instance; movable, not copyable.
 class VmtGenerator {
@@ -73,6 +130,12 @@ public:
     VmtGenerator(std::uint32_t seed, const VmtConfig& cfg, int device = 0) {
         cfg.validate();
         check(vmt_create(seed, cfg.lanes, cfg.jump_exponent, device, &h_));
+    }
+    // VmtGenerator(seed, cfg, jump_matrix) (engine.hpp:162-163): matrix de-phasing
+    VmtGenerator(std::uint32_t seed, const VmtConfig& cfg, const F2Matrix& jump_matrix, int device = 0) {
+        cfg.validate();
+        check(vmt_create_from_matrix(seed, cfg.lanes, jump_matrix.dim() ? jump_matrix.data().data() : nullptr,
+                                     cfg.jump_exponent, device, &h_));
     }
     // lane count 1 needs no jump (engine.hpp:164-167)
     explicit VmtGenerator(std::uint32_t seed) : VmtGenerator(seed, VmtConfig(1, QueryMode::kSingle, 0)) {}
@@ -139,6 +202,9 @@ public:
     static constexpr std::size_t buffer_words = 16;
     VmtEngine(std::uint32_t seed, unsigned jump_exponent, int device = 0)
         : VmtGenerator(seed, VmtConfig(M, QueryMode::kSingle, jump_exponent), device) {}
+    // the reference's constructor (engine.hpp:54): de-phase with B = jump_matrix
+    VmtEngine(std::uint32_t seed, const F2Matrix& jump_matrix, unsigned jump_exponent, int device = 0)
+        : VmtGenerator(seed, VmtConfig(M, QueryMode::kSingle, jump_exponent), jump_matrix, device) {}
     // library-default (full-period) de-phasing on device 0; VmtEngine<1>(seed)
     // is engine.hpp:66-68
     explicit VmtEngine(std::uint32_t seed)

@@ -206,6 +206,9 @@ class RefLib:
         lib.vref_read_jump_matrix_file.argtypes = [c.c_char_p, c.c_void_p, c.POINTER(c.c_uint),
                                                    c.POINTER(c.c_uint)]
         lib.vref_dephased_states_file.argtypes = [c.c_uint32, c.c_uint, c.c_char_p, _u32p]
+        lib.vref_regularized_gamma_q.argtypes = [c.c_double, c.c_double, c.POINTER(c.c_double)]
+        lib.vref_stat_report.argtypes = [c.c_uint32, c.c_uint, c.c_uint, c.c_uint64, c.c_int,
+                                         c.POINTER(c.c_double), c.POINTER(c.c_double), c.POINTER(c.c_int)]
         self.lib = lib
 
     @staticmethod
@@ -275,6 +278,18 @@ class RefLib:
         out = np.empty(624 * lanes, np.uint32)
         self._ok(self.lib.vref_dephased_states_file(seed, lanes, os.fsencode(path), out), "dephased_states_file")
         return out.reshape(lanes, 624)
+
+    def regularized_gamma_q(self, a, x):
+        out = ctypes.c_double()
+        self._ok(self.lib.vref_regularized_gamma_q(a, x, ctypes.byref(out)), "regularized_gamma_q")
+        return out.value
+
+    def stat_report(self, seed, lanes, q, count, which):
+        """(statistic, p_value, pass) of monobit (which=0) / chi2_bytes (1)."""
+        st, p, ok = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+        self._ok(self.lib.vref_stat_report(seed, lanes, q, count, which, ctypes.byref(st), ctypes.byref(p),
+                                           ctypes.byref(ok)), "stat_report")
+        return st.value, p.value, bool(ok.value)
 
     def run_benchmark(self, lanes, mode, count, seed, q):
         s = ctypes.c_double()

@@ -12,6 +12,7 @@
 //   mat_mul / transition F  proj/src/f2_matrix.cpp:138-228
 //   run_benchmark           proj/src/bench.cpp:99-120
 //   .vmtj files             proj/src/jump_file.cpp:117-209
+//   monobit / chi2_bytes    proj/src/stats.cpp:65-107
 // Error mapping: invalid_argument -> -1, logic_error -> -2, other -> -3.
 
 #include <atomic>
@@ -30,6 +31,7 @@
 #include "vmt19937/jump.hpp"
 #include "vmt19937/jump_file.hpp"
 #include "vmt19937/lane_ops.hpp"
+#include "vmt19937/stats.hpp"
 
 using namespace vmt19937;
 
@@ -329,6 +331,28 @@ int vref_dephased_states_file(std::uint32_t seed, unsigned lanes, const char* pa
         auto st = make_dephased_states(Mt19937(seed), JumpSpec{m.exponent, lanes}, m.matrix);
         for (unsigned t = 0; t < lanes; ++t)
             std::memcpy(out + std::size_t(t) * 624, st[t].words().data(), 624 * 4);
+    });
+}
+
+// detail::regularized_gamma_q (stats.cpp:52-60).
+int vref_regularized_gamma_q(double a, double x, double* out) {
+    return guarded([&] { *out = detail::regularized_gamma_q(a, x); });
+}
+
+// monobit (which = 0) / chi2_bytes (which = 1) over the first `count` words
+// of VmtGenerator(seed, VmtConfig(lanes, kSingle, q), F^(2^q)).next_u32, the
+// CLI `stat` wiring (vmt19937_main.cpp:203-214).
+int vref_stat_report(std::uint32_t seed, unsigned lanes, unsigned q, std::uint64_t count, int which,
+                     double* statistic, double* p_value, int* pass) {
+    return guarded([&] {
+        auto gen = lanes == 1 ? std::make_shared<VmtGenerator>(seed)
+                              : std::make_shared<VmtGenerator>(seed, VmtConfig(lanes, QueryMode::kSingle, q),
+                                                               transition_power(q));
+        WordSource src = [gen] { return gen->next_u32(); };
+        const StatReport r = which == 0 ? monobit(src, count) : chi2_bytes(src, count);
+        *statistic = r.statistic;
+        *p_value = r.p_value;
+        *pass = r.pass ? 1 : 0;
     });
 }
 

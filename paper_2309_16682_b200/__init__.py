@@ -33,7 +33,8 @@ __all__ = [
     "InvalidArgument", "LogicError", "VMT_F32_24", "VMT_F64_32", "VMT_F64_REAL3", "VMT_F64_RES53",
     "KEFFECTIVE_BITS", "KSTATE_LEN", "MATRIX_DIM", "MATRIX_ROW_WORDS", "jump_matrix", "jump_matrix_pow2",
     "write_jump_matrix_file", "read_jump_matrix_file", "compute_jump_matrix", "jump_matrix_file_name",
-    "vec_mat_mul", "jump_state_matrix",
+    "vec_mat_mul", "jump_state_matrix", "StatReport", "monobit", "chi2_bytes", "stat_counts",
+    "regularized_gamma_q", "K_SIGNIFICANCE",
 ]
 
 KSTATE_LEN = 624
@@ -279,6 +280,13 @@ class VmtGenerator:
         check(lib.vmt_last_timings(self._h, ctypes.byref(a), ctypes.byref(b)))
         return a.value, b.value
 
+    def stat_counts(self, n: int, stream=None) -> tuple[int, np.ndarray]:
+        """Consumes the next n words without storing them: (one bits, counts
+        of the 256 byte values) -- the fused histogram consumer."""
+        out = np.zeros(257, np.uint64)
+        check(lib.vmt_stat_counts(self._h, n, out.ctypes.data, stream))
+        return int(out[0]), out[1:].copy()
+
     def stats(self) -> dict:
         vals = [ctypes.c_uint64() for _ in range(4)]
         check(lib.vmt_stats(self._h, *[ctypes.byref(v) for v in vals]))
@@ -422,3 +430,46 @@ def jump_state_matrix(states, rows, device: int = 0):
         raise InvalidArgument(_capi.VMT_EINVAL, f"matrix must have {MATRIX_WORDS} uint64 words")
     check(lib.vmt_jump_states_matrix(s.ctypes.data, s.shape[0], addr, out.ctypes.data, device, None))
     return out
+
+
+# ---- statistical smoke tests (stats.hpp) ---------------------------------------
+K_SIGNIFICANCE = 0.001  # stats.hpp:24
+
+
+class StatReport:
+    """stats.hpp:13-20."""
+
+    def __init__(self, name: str, samples: int, statistic: float, p_value: float, passed: bool):
+        self.name, self.samples, self.statistic, self.p_value = name, samples, statistic, p_value
+        self.pass_ = passed
+
+    def __repr__(self) -> str:
+        return (f"StatReport({self.name}, samples={self.samples}, statistic={self.statistic!r}, "
+                f"p={self.p_value!r}, {'PASS' if self.pass_ else 'FAIL'})")
+
+
+def _report(fn, gen: "VmtGenerator", count: int) -> StatReport:
+    r = _capi.StatReportC()
+    check(fn(gen._h, count, ctypes.byref(r)))
+    return StatReport(r.name.decode(), r.samples, r.statistic, r.p_value, bool(r.pass_))
+
+
+def monobit(gen: "VmtGenerator", count: int) -> StatReport:
+    """monobit (stats.cpp:65-81) over the next `count` words of gen."""
+    return _report(lib.vmt_monobit, gen, count)
+
+
+def chi2_bytes(gen: "VmtGenerator", count: int) -> StatReport:
+    """chi2_bytes (stats.cpp:83-107) over the next `count` words of gen."""
+    return _report(lib.vmt_chi2_bytes, gen, count)
+
+
+def stat_counts(gen: "VmtGenerator", n: int) -> tuple[int, np.ndarray]:
+    return gen.stat_counts(n)
+
+
+def regularized_gamma_q(a: float, x: float) -> float:
+    """detail::regularized_gamma_q (stats.cpp:52-60)."""
+    out = ctypes.c_double()
+    check(lib.vmt_regularized_gamma_q(a, x, ctypes.byref(out)))
+    return out.value

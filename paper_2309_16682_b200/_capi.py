@@ -26,8 +26,14 @@ EXPORTS = [
     "vmt_status_string", "vmt_last_error", "vmt_version",
     "vmt_jump_matrix", "vmt_jump_matrix_pow2", "vmt_write_jump_matrix_file", "vmt_read_jump_matrix_file",
     "vmt_compute_jump_matrix_file", "vmt_vec_mat_mul", "vmt_jump_states_matrix", "vmt_create_from_matrix",
-    "vmt_create_from_file",
+    "vmt_create_from_file", "vmt_stat_counts", "vmt_monobit", "vmt_chi2_bytes", "vmt_regularized_gamma_q",
 ]
+
+
+class StatReportC(ctypes.Structure):
+    """vmt_stat_report (StatReport, stats.hpp:13-20)."""
+    _fields_ = [("name", ctypes.c_char_p), ("samples", ctypes.c_uint64), ("statistic", ctypes.c_double),
+                ("p_value", ctypes.c_double), ("pass_", ctypes.c_int)]
 
 
 class VmtError(RuntimeError):
@@ -98,6 +104,10 @@ def _load() -> ctypes.CDLL:
                                              c.c_void_p]),
         "vmt_create_from_matrix": (c.c_int, [c.c_uint32, c.c_uint, c.c_void_p, c.c_uint, c.c_int, c.POINTER(H)]),
         "vmt_create_from_file": (c.c_int, [c.c_uint32, c.c_uint, c.c_char_p, c.c_int, c.POINTER(H)]),
+        "vmt_stat_counts": (c.c_int, [H, c.c_uint64, c.c_void_p, c.c_void_p]),
+        "vmt_monobit": (c.c_int, [H, c.c_uint64, c.POINTER(StatReportC)]),
+        "vmt_chi2_bytes": (c.c_int, [H, c.c_uint64, c.POINTER(StatReportC)]),
+        "vmt_regularized_gamma_q": (c.c_int, [c.c_double, c.c_double, c.POINTER(c.c_double)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -16,7 +16,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libvmt19937_b200.so")
-SOURCES = ["vmt_capi.cu", "gf2poly.cpp"]
+SOURCES = ["vmt_capi.cu", "gf2poly.cpp", "variants_l32a.cu", "variants_l32b.cu", "variants_l16a.cu",
+           "variants_l16b.cu", "variants_l8.cu", "variants_small.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -39,6 +40,15 @@ def _fingerprint() -> str:
     return h.hexdigest()
 
 
+def _compile_cmds(objdir: str) -> list[tuple[list[str], str]]:
+    common = [_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-c"]
+    out = []
+    for src in SOURCES:
+        obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
+        out.append(([*common, os.path.join(CSRC, src), "-o", obj], obj))
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     stamp = LIB + ".stamp"
     fp = _fingerprint()
@@ -46,14 +56,29 @@ def build(force: bool = False, verbose: bool = False) -> str:
         with open(stamp) as f:
             if f.read().strip() == fp:
                 return LIB
-    cmd = [_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
-           "-shared", "-cudart", "static", "-o", LIB + ".tmp",
-           *[os.path.join(CSRC, s) for s in SOURCES], "-lpthread"]
+    objdir = os.path.join(PKG, "_build")
+    os.makedirs(objdir, exist_ok=True)
+    jobs = _compile_cmds(objdir)
+    # one nvcc per translation unit, all in parallel (the kernel instantiations
+    # are split by lane count in variants_*.cu for this)
+    procs = []
+    for cmd, _ in jobs:
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        procs.append(subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
+    errs = []
+    for p in procs:
+        o, _ = p.communicate()
+        if p.returncode != 0:
+            errs.append(" ".join(p.args) + "\n" + o)
+    if errs:
+        raise RuntimeError("nvcc failed:\n" + "\n".join(errs))
+    link = [_nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", LIB + ".tmp", *[o for _, o in jobs], "-lpthread"]
     if verbose:
-        print(" ".join(cmd), flush=True)
-    out = subprocess.run(cmd, capture_output=True, text=True)
+        print(" ".join(link), flush=True)
+    out = subprocess.run(link, capture_output=True, text=True)
     if out.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + out.stdout + out.stderr)
+        raise RuntimeError("nvcc link failed:\n" + out.stdout + out.stderr)
     os.replace(LIB + ".tmp", LIB)
     with open(stamp, "w") as f:
         f.write(fp)

@@ -23,6 +23,7 @@
 #include "../../include/vmt19937_b200.h"
 #include "gf2poly.hpp"
 #include "vmt_kernels.cuh"
+#include "vmt_variants.hpp"
 
 using namespace vmt_b200;
 
@@ -86,62 +87,15 @@ unsigned log2u(unsigned L) {
 }
 
 // ---------------------------------------------------------------- kernels --
-using GenFn = void (*)(GenParams);
-
-struct Variant {
-    int id = 0, L = 0, G = 0, R = 0, VW = 0, W = 0, NT = 0;
-    bool tma = false;
-    int smem[6] = {};
-    GenFn fn[6][2] = {};
-};
-
-template <int LT, int G, int R, int VW, int W, bool TMA, int MODE>
-void fill_mode(Variant& v) {
-    v.fn[MODE][0] = vmt_gen_kernel<LT, G, R, VW, W, TMA, MODE, false>;
-    v.fn[MODE][1] = vmt_gen_kernel<LT, G, R, VW, W, TMA, MODE, true>;
-    v.smem[MODE] = GenShape<G, R, VW, W, TMA>::template smem<MODE>();
-}
-
-// LT = lanes of the stream, G = lanes per CTA (LT/G CTAs per chunk)
-template <int LT, int G, int R, int VW, int W = 208, bool TMA = false>
-Variant make_variant(int id) {
-    Variant v;
-    v.id = id;
-    v.L = LT;
-    v.G = G;
-    v.R = R;
-    v.VW = VW;
-    v.W = W;
-    v.tma = TMA;
-    v.NT = GenShape<G, R, VW, W, TMA>::NT;
-    fill_mode<LT, G, R, VW, W, TMA, MODE_U32>(v);
-    fill_mode<LT, G, R, VW, W, TMA, MODE_XOR>(v);
-    fill_mode<LT, G, R, VW, W, TMA, MODE_F32>(v);
-    fill_mode<LT, G, R, VW, W, TMA, MODE_F64>(v);
-    fill_mode<LT, G, R, VW, W, TMA, MODE_F64_REAL3>(v);
-    fill_mode<LT, G, R, VW, W, TMA, MODE_F64_RES53>(v);
-    return v;
-}
-
-// Kernel shape variants (vmt_set_tuning): run length R = consecutive words
-// per thread per window, VW = lanes per thread, W = window, G = lanes per
-// CTA, TMA = window output staged in shared memory and written by one bulk
-// copy. The first entry per lane count is the default.
-//   id 3: R=13 VW=2   id 1: R=13 VW=4   id 4: R=13 VW=1   id 5: R=1 VW=4
-//   id 6: R=13 VW=2 W=104 TMA bulk stores
-//   id 7: R=13 VW=2 G=8 (lane groups of 8)   id 8: R=13 VW=2 G=16
+// Kernel shape variants (vmt_variants.hpp; instantiated in variants_*.cu).
 const Variant& pick_variant(unsigned L, int variant) {
-    static const std::vector<Variant> table = {
-        make_variant<32, 32, 13, 2>(3), make_variant<32, 32, 13, 4>(1), make_variant<32, 32, 13, 1>(4),
-        make_variant<32, 32, 13, 2, 104, true>(6), make_variant<32, 8, 13, 2>(7), make_variant<32, 16, 13, 2>(8),
-        make_variant<16, 16, 13, 2>(3), make_variant<16, 16, 13, 4>(1), make_variant<16, 16, 13, 1>(4),
-        make_variant<16, 16, 1, 4>(5), make_variant<16, 16, 13, 2, 104, true>(6), make_variant<16, 8, 13, 2>(7),
-        make_variant<8, 8, 13, 2>(3), make_variant<8, 8, 13, 4>(1), make_variant<8, 8, 13, 1>(4),
-        make_variant<8, 8, 1, 4>(5),
-        make_variant<4, 4, 13, 1>(4), make_variant<4, 4, 1, 4>(5),
-        make_variant<2, 2, 13, 1>(4), make_variant<2, 2, 1, 2>(5),
-        make_variant<1, 1, 1, 1>(5),
-    };
+    static const std::vector<Variant> table = [] {
+        std::vector<Variant> t;
+        for (auto part : {variants_l32a, variants_l32b, variants_l16a, variants_l16b, variants_l8, variants_small})
+            for (const Variant& v : part())
+                t.push_back(v);
+        return t;
+    }();
     for (const Variant& v : table)
         if (v.L == (int)L && (variant == 0 || v.id == variant))
             return v;
@@ -434,6 +388,7 @@ struct vmt_generator {
     cudaStream_t side = nullptr;     // prefetch stream
     cudaEvent_t ev_chunks = nullptr, ev_pref = nullptr;
     DevBuf<std::uint32_t> partials;  // per-CTA xor partials
+    DevBuf<unsigned long long> stat_partials; // per-CTA MODE_STATS partials [grid][257]
     DevBuf<std::uint32_t> scratch;   // device staging for host destinations
     DevBuf<std::uint64_t> tmp_poly;
     DevBuf<long long> jsrc, jdst;
@@ -611,7 +566,7 @@ std::uint64_t plan_chunks(unsigned L, std::uint64_t n, std::uint64_t c_max, int 
 
 // Core: GPU-produces stream words [h->gpos, h->gpos + n) into `out` in the
 // representation of `mode` (out == nullptr only for MODE_XOR). Advances gpos.
-void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaStream_t st, std::uint32_t* xor_out_dev) {
+void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaStream_t st, void* reduce_out_dev) {
     if (n == 0)
         return;
     const std::uint64_t P0 = h->gpos, P1 = h->gpos + n;
@@ -625,7 +580,7 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     // of stream word g lives at out + (g - P0).
     const int esz = (mode == MODE_U32 || mode == MODE_F32 || mode == MODE_XOR) ? 4 : 8;
     bool vec = false;
-    if (mode != MODE_XOR && mode != MODE_F64_RES53) {
+    if (mode != MODE_XOR && mode != MODE_STATS && mode != MODE_F64_RES53) {
         const int V = v.G >= v.VW ? v.VW : v.G;
         const std::uintptr_t a = reinterpret_cast<std::uintptr_t>(out);
         const std::uint64_t e = (std::uint64_t)(a / (std::uintptr_t)esz);
@@ -702,10 +657,13 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
         VMT_CUDA(cudaEventRecord(h->ev[1], st));
     if (mode == MODE_XOR)
         h->partials.reserve(grid);
+    if (mode == MODE_STATS)
+        h->stat_partials.reserve(grid * kStatWords);
     GenParams p{};
     p.chunk_states = h->chunks.p;
     p.out = out;
     p.xor_partials = h->partials.p;
+    p.stats_partials = h->stat_partials.p;
     p.save_state = h->next.p;
     p.first_block = b0;
     p.end_block = b1;
@@ -744,7 +702,13 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
         h->ev_valid = true;
     }
     if (mode == MODE_XOR) {
-        vmt_xor_reduce_kernel<<<1, 256, 0, st>>>(h->partials.p, (int)grid, xor_out_dev);
+        vmt_xor_reduce_kernel<<<1, 256, 0, st>>>(h->partials.p, (int)grid, static_cast<std::uint32_t*>(reduce_out_dev));
+        VMT_CUDA(cudaGetLastError());
+        h->cnt.other += 1;
+    }
+    if (mode == MODE_STATS) {
+        vmt_stats_reduce_kernel<<<1, 288, 0, st>>>(h->stat_partials.p, (int)grid,
+                                                   static_cast<unsigned long long*>(reduce_out_dev));
         VMT_CUDA(cudaGetLastError());
         h->cnt.other += 1;
     }
@@ -1361,3 +1325,5 @@ int vmt_version(void) { return 100; }
 
 // GF(2) jump-matrix path: .vmtj files, vec_mat_mul, matrix de-phasing.
 #include "capi_matrix.inl"
+// Fused statistics consumer: monobit / chi2_bytes counts in MODE_STATS.
+#include "capi_stats.inl"

@@ -43,12 +43,17 @@ enum GenMode : int {
     MODE_F64_REAL3 = 4, // (x + 0.5) * 2^-32 in (0,1)      (stats.cpp:118)
     MODE_F64_RES53 = 5, // ((a>>5)*2^26 + (b>>6)) * 2^-53  (two words per value)
     MODE_BENCH_TEMPER_XOR = 6, // scratch/ microbenchmarks only (not reachable from the C ABI)
+    MODE_STATS = 7,     // fused statistics consumer, nothing stored: one-bit count (monobit,
+                        // stats.cpp:65-81) + byte-value histogram (chi2_bytes, stats.cpp:83-107)
 };
+constexpr int kModes = 8;
+constexpr int kStatWords = 257; // MODE_STATS partial per CTA: ones, count[256]
 
 struct GenParams {
     const std::uint32_t* chunk_states; // [C][624][L] interleaved boundary states
     void* out;                         // element of stream word pos_begin (per-chunk offset in batch mode)
     std::uint32_t* xor_partials;       // [gridDim.x] (MODE_XOR)
+    unsigned long long* stats_partials; // [gridDim.x][257] (MODE_STATS)
     std::uint32_t* save_state;         // [624][L] boundary state at save_block (nullable)
     unsigned long long first_block;    // absolute block of chunk 0
     unsigned long long end_block;      // exclusive

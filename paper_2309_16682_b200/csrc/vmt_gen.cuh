@@ -90,9 +90,15 @@ struct GenShape {
     __host__ __device__ static constexpr int stage_bytes() {
         return (TMA && staged_mode<MODE>()) ? W * L * elem_bytes<MODE>() : 0;
     }
+    // MODE_STATS: one 256-bin byte histogram per warp (fewer bank collisions
+    // between warps' shared-memory atomics)
+    template <int MODE>
+    __host__ __device__ static constexpr int hist_bytes() {
+        return MODE == MODE_STATS ? ((NT + 31) / 32) * 256 * 4 : 0;
+    }
     template <int MODE>
     __host__ __device__ static constexpr int smem() {
-        return RING_BYTES + stage_bytes<MODE>() + (stage_bytes<MODE>() ? 16 : 0); // + mbarrier
+        return RING_BYTES + stage_bytes<MODE>() + (stage_bytes<MODE>() ? 16 : 0) + hist_bytes<MODE>(); // + mbarrier
     }
     // CTAs per SM that shared memory allows (227 KB usable, 1 KB reserved per CTA)
     template <int MODE>
@@ -193,6 +199,7 @@ struct StageCtl {
     unsigned phase;   // mbarrier completions consumed so far
     bool prev_staged; // a bulk copy of buf is outstanding (not yet confirmed read)
     bool pending;     // tid 0's view of the same
+    std::uint32_t* hist; // MODE_STATS: this warp's byte histogram
 };
 
 // One window of one thread: R new words of V lanes. base: slot of x_p for
@@ -230,7 +237,7 @@ __device__ __forceinline__ void gen_window(std::uint32_t* ring, int base, int a,
     for (int i = 0; i < R; ++i)
         VecT<V>::get(*reinterpret_cast<const VT*>(ring + (a + i) * L + q * V), M[i]);
     E* o = nullptr;
-    if (MODE != MODE_XOR && MODE != MODE_BENCH_TEMPER_XOR && !STAGE) {
+    if (MODE != MODE_XOR && MODE != MODE_BENCH_TEMPER_XOR && MODE != MODE_STATS && !STAGE) {
         const unsigned long long rel = g0 - p.pos_begin;
         o = static_cast<E*>(out) + (MODE == MODE_F64_RES53 ? (rel >> 1) : rel);
     }
@@ -255,6 +262,21 @@ __device__ __forceinline__ void gen_window(std::uint32_t* ring, int base, int a,
                 const unsigned long long g = g0 + (unsigned long long)i * LT + v;
                 if (FULL || (g >= p.pos_begin && g < p.pos_end))
                     acc[v] ^= nw[v];
+            }
+        } else if (MODE == MODE_STATS) {
+            // acc[0]: one bits of this window's words (folded into 64 bits per
+            // window by the caller); bytes into the warp's histogram
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                const unsigned long long g = g0 + (unsigned long long)i * LT + v;
+                if (FULL || (g >= p.pos_begin && g < p.pos_end)) {
+                    const std::uint32_t t = temper(nw[v]);
+                    acc[0] += __popc(t);
+                    atomicAdd(sc.hist + (t & 0xFFu), 1u);
+                    atomicAdd(sc.hist + ((t >> 8) & 0xFFu), 1u);
+                    atomicAdd(sc.hist + ((t >> 16) & 0xFFu), 1u);
+                    atomicAdd(sc.hist + (t >> 24), 1u);
+                }
             }
         } else if (MODE == MODE_BENCH_TEMPER_XOR) {
             // microbenchmark only: full per-word work of the store path minus the store
@@ -360,6 +382,8 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::NT, GenShape<L, R,
     sc.phase = 0;
     sc.prev_staged = false;
     sc.pending = false;
+    sc.hist = reinterpret_cast<std::uint32_t*>(reinterpret_cast<unsigned char*>(ring) + S::RING_BYTES) +
+              (MODE == MODE_STATS ? (tid >> 5) * 256 : 0);
     // bulk copies need the window's destination 16-byte aligned
     const bool tma_ok =
         kStaged &&
@@ -377,6 +401,14 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::NT, GenShape<L, R,
     constexpr bool kFold = MODE == MODE_XOR || MODE == MODE_BENCH_TEMPER_XOR;
     if (kFold && tid == 0)
         red = 0;
+    __shared__ unsigned long long ones_red;
+    if (MODE == MODE_STATS) {
+        std::uint32_t* h0 = reinterpret_cast<std::uint32_t*>(reinterpret_cast<unsigned char*>(ring) + S::RING_BYTES);
+        for (int i = tid; i < S::template hist_bytes<MODE>() / 4; i += S::NT)
+            h0[i] = 0;
+        if (tid == 0)
+            ones_red = 0;
+    }
     if (kStaged && tid == 0)
         mbar_init(sc.bar, 1);
     __syncthreads();
@@ -387,6 +419,7 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::NT, GenShape<L, R,
         acc[v] = 0;
     constexpr unsigned long long bw = (unsigned long long)kN * LT;
     constexpr unsigned long long ww = (unsigned long long)W * LT; // stream words per window (all lanes)
+    unsigned long long ones = 0; // MODE_STATS
     const bool save_here = p.save_state != nullptr && (!batch || chunk == 0);
     int blk_base_slot = 0; // slot of x_{624 r} for the current block r (= 624 r mod RING)
     constexpr int kWins = kN / W;
@@ -427,6 +460,10 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::NT, GenShape<L, R,
                 gen_window<LT, L, R, VW, W, MODE, VEC, false, false, kHist>(ring, base, a, wsl, q, rho, g0, p, out,
                                                                             acc, sc, tid, Hw);
             __syncthreads();
+            if (MODE == MODE_STATS) {
+                ones += acc[0];
+                acc[0] = 0;
+            }
             if (kStaged) {
                 if (staged && tid == 0) {
                     // all threads' staging writes (generic proxy) -> bulk copy (async proxy)
@@ -472,6 +509,22 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::NT, GenShape<L, R,
         __syncthreads();
         if (tid == 0)
             p.xor_partials[blockIdx.x] = red; // untempered; tempered by the reduce kernel
+    }
+    if (MODE == MODE_STATS) {
+        // (every window ended with a barrier: the histograms are complete)
+        atomicAdd(&ones_red, ones);
+        const std::uint32_t* h0 =
+            reinterpret_cast<const std::uint32_t*>(reinterpret_cast<unsigned char*>(ring) + S::RING_BYTES);
+        unsigned long long* dst = p.stats_partials + (unsigned long long)blockIdx.x * kStatWords;
+        for (int b = tid; b < 256; b += S::NT) {
+            unsigned long long c = 0;
+            for (int w = 0; w < S::template hist_bytes<MODE>() / 1024; ++w)
+                c += h0[w * 256 + b];
+            dst[1 + b] = c;
+        }
+        __syncthreads();
+        if (tid == 0)
+            dst[0] = ones_red;
     }
 }
 

@@ -325,4 +325,15 @@ __global__ void vmt_xor_reduce_kernel(const std::uint32_t* partials, int n, std:
     }
 }
 
+// MODE_STATS: out[j] = sum over CTAs of partials[cta][j], j < 257.
+__global__ void vmt_stats_reduce_kernel(const unsigned long long* partials, int n, unsigned long long* out) {
+    const int j = threadIdx.x;
+    if (j >= kStatWords)
+        return;
+    unsigned long long s = 0;
+    for (int i = 0; i < n; ++i)
+        s += partials[(long long)i * kStatWords + j];
+    out[j] = s;
+}
+
 } // namespace vmt_b200

@@ -137,6 +137,19 @@ int main() {
         require(g.next_u32() == 3499211612u, "first output");
         return std::string("q=19932");
     });
+    criterion("reference constructor VmtEngine<M>(seed, F2Matrix, q) + .vmtj round trip", [] {
+        const unsigned q = 10;
+        const F2Matrix B = jump_matrix_pow2(q);
+        const std::string path = "/tmp/acceptance_b200_" + jump_matrix_file_name(q);
+        compute_jump_matrix(q, path);
+        const LoadedJumpMatrix m = read_jump_matrix_file(path);
+        std::remove(path.c_str());
+        require(m.exponent == q && m.matrix == B, "file round trip");
+        VmtEngine<8> a(4242, m.matrix, m.exponent), b(4242, q);
+        for (int i = 0; i < 20000; ++i)
+            require(a.next_u32() == b.next_u32(), "matrix vs polynomial de-phasing at " + std::to_string(i));
+        return std::string("q=10, 20000 words");
+    });
     std::printf("%d failure(s)\n", failures);
     return failures;
 }

@@ -11,7 +11,7 @@ Sources:
   polynomials x^(2^q) mod P, q = 19932..19936, by plain repeated squaring
   (with the period check x^(2^19937) == x).
 
-Usage: python tests/golden/make_golden.py [--skip-ladder] [--only vmtj]
+Usage: python tests/golden/make_golden.py [--skip-ladder] [--only vmtj|stats]
 (--only SECTION recomputes one section into the existing golden.json)
 """
 from __future__ import annotations
@@ -66,6 +66,30 @@ def vmtj_section(r: RefLib, out: dict) -> None:
     out["vmtj"] = files
 
 
+STAT_CASES = ((5489, 4, 10, 1000000), (5489, 4, 20, 4000000), (5489, 16, 16, 1 << 22), (42, 8, 16, 3000017), (1, 1, 0, 1000000))
+
+
+def stats_section(r: RefLib, out: dict) -> None:
+    """monobit / chi2_bytes reports of the reference (stats.cpp:65-107) on
+    VmtGenerator streams, the counts behind them (numpy over the reference's
+    stream), and detail::regularized_gamma_q on a grid of (dof, statistic)."""
+    cases = []
+    for seed, lanes, q, count in STAT_CASES:
+        v = r.engine_stream(seed, lanes, q, count)
+        ones = int(np.unpackbits(v.view(np.uint8)).sum())
+        bins = np.bincount(v.view(np.uint8), minlength=256)
+        c = {"seed": seed, "lanes": lanes, "q": q, "count": count, "ones": ones, "bins": [int(b) for b in bins]}
+        for which, name in ((0, "monobit"), (1, "chi2_bytes")):
+            st, pv, ok = r.stat_report(seed, lanes, q, count, which)
+            c[name] = {"statistic": st, "p_value": pv, "pass": ok}
+        cases.append(c)
+    gq = []
+    for dof in (31, 100, 255, 1023):
+        for stat in np.linspace(0.5, 3.0 * dof, 41):
+            gq.append([dof / 2.0, float(stat) / 2.0, r.regularized_gamma_q(dof / 2.0, float(stat) / 2.0)])
+    out["stats"] = {"reports": cases, "gamma_q": gq}
+
+
 def main() -> None:
     skip_ladder = "--skip-ladder" in sys.argv
     if "--only" in sys.argv:
@@ -73,7 +97,7 @@ def main() -> None:
         path = os.path.join(HERE, "golden.json")
         with open(path) as f:
             out = json.load(f)
-        {"vmtj": vmtj_section}[section](RefLib(), out)
+        {"vmtj": vmtj_section, "stats": stats_section}[section](RefLib(), out)
         with open(path, "w") as f:
             json.dump(out, f, indent=1)
         return
@@ -151,6 +175,7 @@ def main() -> None:
     out["period_check"] = "x^(2^19937) == x mod P"
     print(f"full-period polys {time.time() - t0:.1f}s", flush=True)
     vmtj_section(r, out)
+    stats_section(r, out)
 
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(out, f, indent=1)

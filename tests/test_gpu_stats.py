@@ -1,0 +1,87 @@
+"""GPU parity of the fused statistics consumer (north_star "optional fused
+consumer (checksum or histogram)"): one-bit and byte-value
+counts taken inside the generation kernel (nothing stored) against the
+reference's stream, and monobit / chi2_bytes reports against the reference's
+stats.cpp on the same streams."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2309_16682_b200 as V  # noqa: E402
+
+POP8 = np.array([bin(i).count("1") for i in range(256)], np.uint64)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need a CUDA device")
+
+
+def np_counts(words):
+    bins = np.bincount(np.asarray(words, np.uint32).view(np.uint8), minlength=256).astype(np.uint64)
+    return int((bins * POP8).sum()), bins
+
+
+def test_counts_and_reports_match_reference(golden):
+    for c in golden["stats"]["reports"]:
+        g = V.VmtGenerator(c["seed"], V.VmtConfig(c["lanes"], jump_exponent=c["q"]))
+        ones, bins = g.stat_counts(c["count"])
+        assert ones == c["ones"], c
+        assert [int(b) for b in bins] == c["bins"], c
+        for fn, name in ((V.monobit, "monobit"), (V.chi2_bytes, "chi2_bytes")):
+            r = fn(V.VmtGenerator(c["seed"], V.VmtConfig(c["lanes"], jump_exponent=c["q"])), c["count"])
+            ref = c[name]
+            assert r.name == name and r.samples == c["count"]
+            assert r.statistic == ref["statistic"], (name, c["lanes"], r.statistic, ref["statistic"])
+            assert r.p_value == pytest.approx(ref["p_value"], rel=1e-12, abs=1e-300), (name, c["lanes"])
+            assert r.pass_ == ref["pass"], (name, c["lanes"])
+
+
+def test_counts_continue_the_stream(oracle):
+    """Counting consumes words like a fill: mixed with next_u32 / fills and at
+    ragged positions the counted words are exactly the next n of the stream."""
+    L, q = 16, 12
+    lanes = oracle.dephased_states(9, L, oracle.x_pow2_mod(q))
+    total = 3 * 624 * L + 777
+    ref = oracle.vmt_stream(lanes, 0, total + 200000)
+    g = V.VmtEngine(L, 9, q)
+    pos = 0
+    for _ in range(5):
+        assert g.next_u32() == ref[pos]
+        pos += 1
+    for n in (13, 624 * L - 1, 2 * 624 * L + 5, 100003):
+        ones, bins = g.stat_counts(n)
+        eo, eb = np_counts(ref[pos:pos + n])
+        assert ones == eo and np.array_equal(bins, eb), n
+        pos += n
+    out = np.empty(50, np.uint32)
+    g.fill_u32(out)
+    assert np.array_equal(out, ref[pos:pos + 50])
+
+
+def test_undersized_samples_rejected():
+    g = V.VmtEngine(4, 1, 8)
+    with pytest.raises(V.InvalidArgument):
+        V.monobit(g, 999999)
+    with pytest.raises(V.InvalidArgument):
+        V.chi2_bytes(g, 3199)
+
+
+@pytest.mark.parametrize("L", [8, 32])
+def test_large_counts_vs_stored_stream(L):
+    """At 2^30 words: the fused counts equal a torch bincount of the same words
+    stored by fill_u32 (size-independent check of the histogram path)."""
+    n = 1 << 30
+    g = V.VmtGenerator(5489, V.VmtConfig(L))
+    ones, bins = g.stat_counts(n)
+    h = V.VmtGenerator(5489, V.VmtConfig(L))
+    buf = torch.empty(n, dtype=torch.uint32, device="cuda")
+    h.fill_u32(buf)
+    tb = torch.bincount(buf.view(torch.uint8), minlength=256).cpu().numpy().astype(np.uint64)
+    del buf
+    assert np.array_equal(bins, tb)
+    assert ones == int((tb * POP8).sum())
+    assert int(bins.sum()) == 4 * n
