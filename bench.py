@@ -5,12 +5,13 @@ Workload (BASELINE.json configs[3], the one the metric is quoted on: "uint32
 random numbers/sec per GPU and whole box (1/2/4/8 B200)"): one VMT19937 stream
 with L = 32 lanes, seed 5489 (init_genrand), lanes de-phased by the library
 default jump-ahead (q = 19937 - log2 32 = 19932), 2^34 uint32 words (64 GiB)
-per step, partitioned into contiguous ranges across the N ranks (strong
-scaling; each rank jumps to its range, no data-path collective). A step is one
-pass over the whole 2^34-word range; consecutive steps generate consecutive
-2^34-word ranges of the stream (so every step pays the chunk-positioning jump
-work, nothing is cached between steps). Output goes to a preallocated HBM
-buffer of the rank's share (64 GiB at N=1 -- larger than L2, no flush needed).
+per rank per step (--scaling weak, the default: rank r owns words
+[r*2^34, (r+1)*2^34) of an N*2^34-word range; --scaling strong splits one
+2^34 range N ways). Each rank jumps to its range; no data-path collective. A
+step is one pass over the range; consecutive steps generate consecutive ranges
+of the stream (so every step pays the chunk-positioning jump work, nothing is
+cached between steps). Output goes to a preallocated HBM buffer of the rank's
+share (64 GiB -- larger than L2, no flush needed).
 
 value    : whole-job uint32/s over all ranks, CUDA events on the launching
            stream, max over ranks (positioning jumps + generation kernels).
@@ -57,6 +58,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the other BASELINE configs (N=1 only)")
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--chunks", type=int, default=0)
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
@@ -210,6 +212,75 @@ def cpu_model():
     except Exception:
         pass
     return "unknown"
+
+
+def extras(dev) -> dict:
+    """The other BASELINE.json configs and the path's side subsystems, timed
+    on the device (CUDA events on the call's stream, inputs/outputs in HBM),
+    one rank, a few seconds in total. These are parity-test cases in tests/;
+    here only their throughput is reported."""
+    import numpy as np
+    import torch
+
+    import paper_2309_16682_b200 as V
+
+    stream = torch.cuda.current_stream(dev)
+
+    def timed(fn, reps=3):
+        fn()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / reps * 1e-3
+
+    out = {}
+    # c1: L=16, seed 5489, full-period de-phasing, 2^26 uint32 (setup excluded, like bench.hpp:27-30)
+    n = 1 << 26
+    buf = torch.empty(n, dtype=torch.uint32, device=dev)
+    g = V.VmtGenerator(5489, V.VmtConfig(16))
+    s = timed(lambda: g.fill_u32(buf))
+    out["c1_L16_2p26_u32"] = {"value": n / s, "unit": "uint32/s", "ms": s * 1e3}
+    # c2: L=8, seed 42, 2^28 -> float32 and float64 in [0,1)
+    n = 1 << 28
+    f32 = torch.empty(n, dtype=torch.float32, device=dev)
+    g = V.VmtGenerator(42, V.VmtConfig(8))
+    s = timed(lambda: g.fill_f32(f32))
+    out["c2_L8_2p28_f32"] = {"value": n / s, "unit": "float32/s", "ms": s * 1e3, "gbs": n * 4 / s / 1e9}
+    del f32
+    f64 = torch.empty(n, dtype=torch.float64, device=dev)
+    s = timed(lambda: g.fill_f64(f64))
+    out["c2_L8_2p28_f64"] = {"value": n / s, "unit": "float64/s", "ms": s * 1e3, "gbs": n * 8 / s / 1e9}
+    del f64
+    # c3: 1024 generators (L=16, seeds 1..1024, full period) x 2^20 words, generator-major,
+    # including the 1024 x 15 de-phasing jumps
+    n = 1 << 20
+    b3 = torch.empty(1024 * n, dtype=torch.uint32, device=dev)
+    s = timed(lambda: V.batch_fill_u32(b3, 1, 1024, 16, n), reps=2)
+    out["c3_1024xL16_2p20_u32"] = {"value": 1024 * n / s, "unit": "uint32/s", "ms": s * 1e3,
+                                   "note": "includes seeding + 15360 full-period de-phasing jumps"}
+    del b3
+    # c5: 4096 states (seeds 1..4096) jumped by 64-bit distances, then 624 outputs each
+    seeds = np.arange(1, 4097, dtype=np.uint32)
+    states = torch.from_numpy(V.seed_states(seeds).view(np.int32)).to(dev).view(torch.uint32)
+    dists = np.random.default_rng(7).integers(0, 2**63, 4096, dtype=np.int64).view(np.uint64)
+    jumped = torch.empty_like(states)
+    s = timed(lambda: V.jump_states(states, dists, out=jumped), reps=2)
+    out["c5_4096_jumps_64bit"] = {"value": 4096 / s, "unit": "state jumps/s", "ms": s * 1e3,
+                                  "note": "8 digit-table polynomial jumps per state (64-bit distance)"}
+    # fused statistics consumer (monobit + chi2 byte histogram), 2^32 words, nothing stored
+    n = 1 << 32
+    g = V.VmtGenerator(5489, V.VmtConfig(32))
+    s = timed(lambda: g.stat_counts(n), reps=2)
+    out["stats_consumer_L32_2p32"] = {"value": n / s, "unit": "uint32/s", "ms": s * 1e3}
+    # full-period jump matrix F^(2^19932) (the reference needs ~50 h of squarings)
+    rows = torch.empty((19937, 312), dtype=torch.uint64, device=dev)
+    s = timed(lambda: V.jump_matrix_pow2(19932, out=rows), reps=2)
+    out["jump_matrix_2p19932"] = {"value": s * 1e3, "unit": "ms", "note": "19937 basis-state polynomial jumps"}
+    return out
 
 
 def run_reference(args):
@@ -404,6 +475,16 @@ def main():
         except Exception as e:  # the reference build is optional on the box
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {e}"}
+    if rank == 0 and world == 1 and not args.no_extras:
+        try:
+            del out
+        except NameError:
+            pass
+        torch.cuda.empty_cache()
+        try:
+            line["other_configs"] = extras(dev)
+        except Exception as e:
+            line["other_configs"] = {"error": f"{type(e).__name__}: {e}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

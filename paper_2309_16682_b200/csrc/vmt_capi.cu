@@ -529,8 +529,8 @@ void reposition(vmt_generator* h, std::uint64_t target, cudaStream_t st) {
 //   t(C) = t_jump((C-1) L) + (n / C) / min(L * r_lane, peak_sm / k),
 // k = ceil(C / sms) chunks sharing the busiest SM, with constants measured on
 // B200: a lane jump costs 0.43 us of whole-GPU
-// throughput with a latency floor of 0.16-0.5 ms, one lane generates ~2.9e8
-// words/s, an SM's store path saturates at ~1.5e12 / 148 words/s. Past one
+// throughput with a latency floor of 0.16-0.5 ms, one lane generates ~3.2e8
+// words/s, an SM's store path saturates at ~1.6e12 / 148 words/s. Past one
 // chunk per SM only whole waves (multiples of sms) are candidates: a partial
 // wave leaves the SMs with one chunk more as the tail.
 std::uint64_t plan_chunks(unsigned L, std::uint64_t n, std::uint64_t c_max, int sms) {
@@ -541,7 +541,7 @@ std::uint64_t plan_chunks(unsigned L, std::uint64_t n, std::uint64_t c_max, int 
         const double floor_s = jobs <= sms * 4.0 ? 0.16e-3 : (jobs <= sms * 16.0 ? 0.37e-3 : 0.0);
         return std::max(floor_s, jobs * per_jump);
     };
-    const double r_lane = 2.9e8, peak_sm = 1.5e12 / 148.0;
+    const double r_lane = 3.2e8, peak_sm = 1.6e12 / 148.0;
     auto t = [&](std::uint64_t C) {
         const double k = (double)((C + sms - 1) / sms);
         return t_jump(double(C - 1) * L) + (double(n) / double(C)) / std::min(L * r_lane, peak_sm / k);

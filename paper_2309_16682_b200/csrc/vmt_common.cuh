@@ -65,8 +65,8 @@ struct GenParams {
     unsigned int lanes;
 };
 
-// ---- per-word arithmetic (hand-scheduled LOP3 forms; SASS: 4 ALU + 1 FMA-pipe
-// op for the twist, 6 ALU + 2 FMA-pipe ops for the temper) -------------------
+// ---- per-word arithmetic (hand-scheduled LOP3 forms; SASS: 3 ALU + 2 FMA-pipe
+// ops for the twist, 6 ALU + 2 FMA-pipe ops for the temper) -----------------
 
 __device__ __forceinline__ std::uint32_t lop3_sel_hi(std::uint32_t hi_src, std::uint32_t lo_src) {
     // (hi_src & 0x80000000) | (lo_src & 0x7FFFFFFF)
@@ -94,14 +94,30 @@ __device__ __forceinline__ std::uint32_t mul_lo(std::uint32_t a, std::uint32_t b
 
 // x_k <- x_{k+m} ^ mulA((x_k & h) | (x_{k+1} & l))   (mt19937.cpp:44, mt19937.hpp:70-72;
 // lane form: lane_ops.hpp:81-85)
+#ifndef VMT_TWIST_FMA_MAG
+#define VMT_TWIST_FMA_MAG 1
+#endif
+__device__ __forceinline__ std::uint32_t mad_lo(std::uint32_t a, std::uint32_t b, std::uint32_t c) {
+    std::uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
 __device__ __forceinline__ std::uint32_t twist(std::uint32_t xk, std::uint32_t xk1, std::uint32_t xm) {
     const std::uint32_t u = lop3_sel_hi(xk, xk1);
+    const std::uint32_t uh = u >> 1;
+#if VMT_TWIST_FMA_MAG
+    // mag = (u & 1) * A = u*A - (u >> 1)*2A: two IMADs on the FMA pipe instead
+    // of a LOP3 + IMAD, so the twist costs 3 ALU-pipe ops (LOP3, SHF, LOP3)
+    const std::uint32_t mag = mad_lo(u, kMatA, mul_lo(uh, 0u - 2u * kMatA));
+#else
     const std::uint32_t mag = mul_lo(xk1 & 1u, kMatA); // odd(u) == odd(x_{k+1}); IMAD on the FMA pipe
-    return xor3(xm, u >> 1, mag);
+#endif
+    return xor3(xm, uh, mag);
 }
 
 // Tempering (mt19937.hpp:61-66; lane form lane_ops.hpp:88-93). Left shifts
-// are multiplies so they issue on the FMA pipe.
+// are multiplies so they issue on the FMA pipe. (Right shifts as the high word
+// of IMAD.WIDE were measured 6% slower: the wide multiply is not FMA-pipe only.)
 __device__ __forceinline__ std::uint32_t temper(std::uint32_t y) {
     y ^= y >> 11;
     y = xor_and<0x9D2C5680u>(y, mul_lo(y, 1u << 7));

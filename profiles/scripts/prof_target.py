@@ -1,0 +1,34 @@
+"""Single-launch targets for `ncu --set full` (one kernel of interest per run).
+
+  gen   : vmt_gen_kernel, store mode, L=32 full period, 2^32 words, 148 chunks
+          (one chunk per SM, the bench's shape; 2^32 instead of 2^34 so ncu's
+          save/restore of the written buffer stays at 16 GiB)
+  jump  : vmt_jump_kernel, the bench's positioning launch (147 x 32 = 4704 jobs)
+  stats : vmt_gen_kernel MODE_STATS (fused monobit + byte histogram), 2^32 words
+  xor   : vmt_gen_kernel MODE_XOR (fused checksum), 2^32 words
+Each target runs its call three times; profile with --launch-skip/-c on the
+kernel name (see profiles/scripts/profile.sh).
+"""
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+import paper_2309_16682_b200 as V  # noqa: E402
+
+what = sys.argv[1]
+n = 1 << 32
+g = V.VmtGenerator(5489, V.VmtConfig(32))
+g.set_tuning(max_chunks=148)
+if what in ("gen", "jump"):
+    buf = torch.empty(n, dtype=torch.uint32, device="cuda")
+    for _ in range(3):
+        g.fill_u32(buf)
+elif what == "stats":
+    for _ in range(3):
+        g.stat_counts(n)
+elif what == "xor":
+    for _ in range(3):
+        g.checksum_xor(n)
+torch.cuda.synchronize()
+print("done", what)
