@@ -358,6 +358,8 @@ def main():
     torch.cuda.synchronize(dev)
 
     clocks = ClockSampler(dev)
+    g.set_profiling(True)  # CUDA events around each step's jump and generation launches
+    g.profile_totals()
     clocks.start()
     s0 = g.stats()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -371,24 +373,15 @@ def main():
     torch.cuda.synchronize(dev)
     clk = clocks.stop()
     s1 = g.stats()
+    fills, jump_tot, gen_tot = g.profile_totals()
+    g.set_profiling(False)
     ms = e0.elapsed_time(e1) / args.steps
     ms = max_over_ranks(ms, dev)
     launches = sum(s1[k] - s0[k] for k in ("gen_launches", "jump_launches", "other_launches"))
-
-    # -- the generation kernel's own duration and the positioning jumps before
-    # it (CUDA events around each on the fill's stream, same steps as timed)
-    def kernel_times():
-        g.set_profiling(True)
-        jumps, gens = [], []
-        for _ in range(args.steps):
-            step()
-            j, gm = g.last_timings()
-            jumps.append(j)
-            gens.append(gm)
-        g.set_profiling(False)
-        return max_over_ranks(statistics.mean(gens), dev), max_over_ranks(statistics.mean(jumps), dev)
-
-    gen_ms, jump_ms = kernel_times()
+    # the generation kernel's own duration and the positioning jumps before
+    # it, from the same timed steps
+    gen_ms = max_over_ranks(gen_tot / max(fills, 1), dev)
+    jump_ms = max_over_ranks(jump_tot / max(fills, 1), dev)
 
     # -- global checksum of one full 2^34 range (config 4 verification)
     g.seek(start)
@@ -454,7 +447,7 @@ def main():
         "per_gpu_value": count / (ms * 1e-3),
         "timing_breakdown_ms": {"gen_kernel": gen_ms, "positioning_jumps": jump_ms,
                                 "note": "CUDA events on the fill's stream around the chunk-positioning jump "
-                                        "launch and the generation launch of each step (back to back)"},
+                                        "launch and the generation launch of every timed step"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": (traffic or {}).get("dram_bytes_per_launch"),
                      "kernel": "vmt_gen_kernel", "peak_source": peak_src,

@@ -192,6 +192,9 @@ int vmt_set_prefetch(vmt_handle h, int enable);
  * returns both durations (ms) of the most recent fill. */
 int vmt_set_profiling(vmt_handle h, int enable);
 int vmt_last_timings(vmt_handle h, float* jump_ms, float* gen_ms);
+/* Sums over every fill recorded since profiling was enabled or since the
+ * previous call (which resets them): fills, positioning-jump ms, generation ms. */
+int vmt_profile_totals(vmt_handle h, uint64_t* fills, double* jump_ms, double* gen_ms);
 
 /* Counters: kernels launched by this handle so far (generation, jump, seed,
  * reduce), and the number of lane-state jumps performed. */

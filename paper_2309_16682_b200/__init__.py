@@ -287,6 +287,13 @@ class VmtGenerator:
         check(lib.vmt_stat_counts(self._h, n, out.ctypes.data, stream))
         return int(out[0]), out[1:].copy()
 
+    def profile_totals(self) -> tuple[int, float, float]:
+        """(fills, positioning-jump ms, generation ms) summed over the fills
+        since profiling was enabled / the previous call; resets the sums."""
+        n, j, gm = ctypes.c_uint64(), ctypes.c_double(), ctypes.c_double()
+        check(lib.vmt_profile_totals(self._h, ctypes.byref(n), ctypes.byref(j), ctypes.byref(gm)))
+        return n.value, j.value, gm.value
+
     def stats(self) -> dict:
         vals = [ctypes.c_uint64() for _ in range(4)]
         check(lib.vmt_stats(self._h, *[ctypes.byref(v) for v in vals]))

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -405,8 +406,13 @@ struct vmt_generator {
     int variant = 0;
     Counters cnt;
     bool profile = false;
-    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr}; // before jumps, before gen, after gen
-    bool ev_valid = false;
+    // profiling: one event triplet per fill (before jumps, before gen, after
+    // gen), folded into running totals when the pool is full or on request
+    std::vector<std::array<cudaEvent_t, 3>> evpool;
+    std::size_t ev_used = 0;
+    std::uint64_t prof_fills = 0;
+    double prof_jump_ms = 0, prof_gen_ms = 0;
+    float last_jump_ms = -1.f, last_gen_ms = -1.f;
 
     cudaStream_t pick(void* s) {
         cudaStream_t st = s ? static_cast<cudaStream_t>(s) : own;
@@ -524,6 +530,37 @@ void reposition(vmt_generator* h, std::uint64_t target, cudaStream_t st) {
     h->cur_block = target;
 }
 
+// Profiling event pool (vmt_set_profiling).
+constexpr std::size_t kProfPool = 1024;
+
+void prof_fold(vmt_generator* h) {
+    for (std::size_t i = 0; i < h->ev_used; ++i) {
+        auto& e = h->evpool[i];
+        VMT_CUDA(cudaEventSynchronize(e[2]));
+        float a = 0, b = 0;
+        VMT_CUDA(cudaEventElapsedTime(&a, e[0], e[1]));
+        VMT_CUDA(cudaEventElapsedTime(&b, e[1], e[2]));
+        h->prof_jump_ms += a;
+        h->prof_gen_ms += b;
+        h->last_jump_ms = a;
+        h->last_gen_ms = b;
+        ++h->prof_fills;
+    }
+    h->ev_used = 0;
+}
+
+cudaEvent_t* prof_next(vmt_generator* h) {
+    if (h->ev_used == kProfPool)
+        prof_fold(h);
+    if (h->ev_used == h->evpool.size()) {
+        std::array<cudaEvent_t, 3> e{};
+        for (auto& x : e)
+            VMT_CUDA(cudaEventCreate(&x));
+        h->evpool.push_back(e);
+    }
+    return h->evpool[h->ev_used++].data();
+}
+
 // Chunk count for a fill of n words: every chunk but the first costs L lane
 // jumps (positioning), every chunk adds generation parallelism. Minimise
 //   t(C) = t_jump((C-1) L) + (n / C) / min(L * r_lane, peak_sm / k),
@@ -571,8 +608,9 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
         return;
     const std::uint64_t P0 = h->gpos, P1 = h->gpos + n;
     const std::uint64_t b0 = P0 / h->bw, b1 = (P1 + h->bw - 1) / h->bw;
-    if (h->profile)
-        VMT_CUDA(cudaEventRecord(h->ev[0], st));
+    cudaEvent_t* pe = h->profile ? prof_next(h) : nullptr;
+    if (pe)
+        VMT_CUDA(cudaEventRecord(pe[0], st));
     const Variant& v = pick_variant(h->L, h->variant);
     const int groups = v.L / v.G; // CTAs per chunk (lane groups)
     const std::uint64_t nb = b1 - b0;
@@ -653,8 +691,8 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
         VMT_CUDA(cudaEventRecord(h->ev_chunks, st));
     }
     const std::uint64_t grid = C * groups;
-    if (h->profile)
-        VMT_CUDA(cudaEventRecord(h->ev[1], st));
+    if (pe)
+        VMT_CUDA(cudaEventRecord(pe[1], st));
     if (mode == MODE_XOR)
         h->partials.reserve(grid);
     if (mode == MODE_STATS)
@@ -697,10 +735,8 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
         h->pref_C = C;
     }
     h->last_end = P1;
-    if (h->profile) {
-        VMT_CUDA(cudaEventRecord(h->ev[2], st));
-        h->ev_valid = true;
-    }
+    if (pe)
+        VMT_CUDA(cudaEventRecord(pe[2], st));
     if (mode == MODE_XOR) {
         vmt_xor_reduce_kernel<<<1, 256, 0, st>>>(h->partials.p, (int)grid, static_cast<std::uint32_t*>(reduce_out_dev));
         VMT_CUDA(cudaGetLastError());
@@ -914,8 +950,8 @@ int vmt_destroy(vmt_handle h) {
             if (h->hsmall)
                 cudaFreeHost(h->hsmall);
             cudaEventDestroy(h->last);
-            for (auto& e : h->ev)
-                if (e)
+            for (auto& t : h->evpool)
+                for (auto& e : t)
                     cudaEventDestroy(e);
             if (h->side) {
                 cudaStreamSynchronize(h->side);
@@ -1266,27 +1302,37 @@ int vmt_set_profiling(vmt_handle h, int enable) {
     return guarded([&] {
         require(h != nullptr, VMT_EINVAL, "null handle");
         DeviceGuard g(h->device);
-        if (enable && !h->ev[0])
-            for (auto& e : h->ev)
-                VMT_CUDA(cudaEventCreate(&e));
+        prof_fold(h);
         h->profile = enable != 0;
-        h->ev_valid = false;
     });
 }
 
 int vmt_last_timings(vmt_handle h, float* jump_ms, float* gen_ms) {
     return guarded([&] {
         require(h != nullptr, VMT_EINVAL, "null handle");
-        require(h->profile && h->ev_valid, VMT_ESTATE, "profiling disabled or no fill recorded");
         DeviceGuard g(h->device);
-        VMT_CUDA(cudaEventSynchronize(h->ev[2]));
-        float a = 0, b = 0;
-        VMT_CUDA(cudaEventElapsedTime(&a, h->ev[0], h->ev[1]));
-        VMT_CUDA(cudaEventElapsedTime(&b, h->ev[1], h->ev[2]));
+        prof_fold(h);
+        require(h->last_gen_ms >= 0.f, VMT_ESTATE, "profiling disabled or no fill recorded");
         if (jump_ms)
-            *jump_ms = a;
+            *jump_ms = h->last_jump_ms;
         if (gen_ms)
-            *gen_ms = b;
+            *gen_ms = h->last_gen_ms;
+    });
+}
+
+int vmt_profile_totals(vmt_handle h, uint64_t* fills, double* jump_ms, double* gen_ms) {
+    return guarded([&] {
+        require(h != nullptr, VMT_EINVAL, "null handle");
+        DeviceGuard g(h->device);
+        prof_fold(h);
+        if (fills)
+            *fills = h->prof_fills;
+        if (jump_ms)
+            *jump_ms = h->prof_jump_ms;
+        if (gen_ms)
+            *gen_ms = h->prof_gen_ms;
+        h->prof_fills = 0;
+        h->prof_jump_ms = h->prof_gen_ms = 0;
     });
 }
 

@@ -111,7 +111,8 @@ __device__ __forceinline__ void jump_pair(std::uint32_t (&Y)[20], const std::uin
 }
 
 #ifndef VMT_JUMP_QUADS
-#define VMT_JUMP_QUADS 0 // 16-way quad switch measured 1.7x slower (code size)
+#define VMT_JUMP_QUADS 0 // 16-way quad switch measured 1.7x slower (code size; a 7-way
+                         // triple switch, 11% fewer LOP3s, measured 1.3x slower too)
 #endif
 __device__ __forceinline__ void jump_group(std::uint32_t (&Y)[20], const std::uint32_t (&A)[20],
                                            const std::uint32_t (&B)[20], unsigned cm) {
@@ -180,7 +181,7 @@ __device__ __forceinline__ void jump_load20(const std::uint32_t* seq, int start,
 // XOR-reduced through shared memory -- SPLIT > 1 trades ~10% extra work for a
 // SPLIT-fold shorter latency when there are few jobs.
 #ifndef VMT_JUMP_MINB
-#define VMT_JUMP_MINB 32
+#define VMT_JUMP_MINB 24 // 77 registers, no spills (32: 64 registers + spills, 4% slower)
 #endif
 template <int SPLIT>
 __global__ void __launch_bounds__(32 * SPLIT, (SPLIT == 1 ? VMT_JUMP_MINB : 32 / SPLIT)) vmt_jump_kernel(JumpParams p) {

@@ -312,3 +312,23 @@ def test_float_conversions_tma_variant(oracle):
     t = torch.empty(n, dtype=torch.float64, device="cuda")
     g.fill_f64(t)
     assert np.array_equal(host(t), u.astype(np.float64) * 2.0 ** -32)
+
+
+def test_profiling_events_cover_every_fill():
+    """vmt_set_profiling / vmt_last_timings / vmt_profile_totals: one event
+    triplet per fill, summed over all fills (bench.py's kernel breakdown)."""
+    g = V.VmtEngine(16, 3, 10)
+    out = dev_u32(1 << 22)
+    with pytest.raises(V.LogicError):
+        g.last_timings()
+    g.set_profiling(True)
+    for _ in range(5):
+        g.fill_u32(out)
+    j, gm = g.last_timings()
+    assert gm > 0 and j >= 0
+    n, jt, gt = g.profile_totals()
+    assert n == 5 and gt >= gm and jt >= 0
+    assert g.profile_totals() == (0, 0.0, 0.0)
+    g.set_profiling(False)
+    g.fill_u32(out)
+    assert g.profile_totals()[0] == 0
