@@ -221,6 +221,13 @@ int vmt_stat_counts(vmt_handle h, uint64_t n, uint64_t* out257, void* stream);
  * VMT_EINVAL like the reference's std::invalid_argument. */
 int vmt_monobit(vmt_handle h, uint64_t count, vmt_stat_report* out);
 int vmt_chi2_bytes(vmt_handle h, uint64_t count, vmt_stat_report* out);
+/* The same reports from counts taken elsewhere (bins256 = byte-value counts). */
+int vmt_monobit_from_counts(uint64_t count, uint64_t ones, vmt_stat_report* out);
+int vmt_chi2_bytes_from_counts(uint64_t count, const uint64_t* bins256, vmt_stat_report* out);
+/* lane_cross_correlation (stats.cpp:109-150) over the next count*lanes words:
+ * lane t's sequence is column t of the combined stream. Needs lanes >= 2
+ * (VMT_EINVAL). Floating point: equal to the reference within 1e-12. */
+int vmt_lane_cross_correlation(vmt_handle h, uint64_t count, vmt_stat_report* out);
 /* detail::regularized_gamma_q (stats.hpp:47-50, stats.cpp:52-60). */
 int vmt_regularized_gamma_q(double a, double x, double* out);
 

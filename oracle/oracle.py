@@ -209,6 +209,11 @@ class RefLib:
         lib.vref_regularized_gamma_q.argtypes = [c.c_double, c.c_double, c.POINTER(c.c_double)]
         lib.vref_stat_report.argtypes = [c.c_uint32, c.c_uint, c.c_uint, c.c_uint64, c.c_int,
                                          c.POINTER(c.c_double), c.POINTER(c.c_double), c.POINTER(c.c_int)]
+        for name in ("vref_lane_corr",):
+            getattr(lib, name).argtypes = [c.c_uint32, c.c_uint, c.c_uint, c.c_uint64, c.POINTER(c.c_double),
+                                           c.POINTER(c.c_double), c.POINTER(c.c_int)]
+        lib.vref_stat_constant.argtypes = [c.c_uint32, c.c_uint64, c.c_int, c.POINTER(c.c_double),
+                                           c.POINTER(c.c_double), c.POINTER(c.c_int)]
         self.lib = lib
 
     @staticmethod
@@ -289,6 +294,18 @@ class RefLib:
         st, p, ok = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
         self._ok(self.lib.vref_stat_report(seed, lanes, q, count, which, ctypes.byref(st), ctypes.byref(p),
                                            ctypes.byref(ok)), "stat_report")
+        return st.value, p.value, bool(ok.value)
+
+    def lane_corr(self, seed, lanes, q, count):
+        st, p, ok = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+        self._ok(self.lib.vref_lane_corr(seed, lanes, q, count, ctypes.byref(st), ctypes.byref(p), ctypes.byref(ok)),
+                 "lane_corr")
+        return st.value, p.value, bool(ok.value)
+
+    def stat_constant(self, word, count, which):
+        st, p, ok = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+        self._ok(self.lib.vref_stat_constant(word, count, which, ctypes.byref(st), ctypes.byref(p),
+                                             ctypes.byref(ok)), "stat_constant")
         return st.value, p.value, bool(ok.value)
 
     def run_benchmark(self, lanes, mode, count, seed, q):

@@ -356,6 +356,41 @@ int vref_stat_report(std::uint32_t seed, unsigned lanes, unsigned q, std::uint64
     });
 }
 
+// lane_cross_correlation over the CLI's per-lane sources (make_dephased_states
+// + regenerate + next_u32, vmt19937_main.cpp:216-229); which = 2 on a
+// constant source pair instead when seed_or_word is used as the word.
+int vref_lane_corr(std::uint32_t seed, unsigned lanes, unsigned q, std::uint64_t count, double* statistic,
+                   double* p_value, int* pass) {
+    return guarded([&] {
+        auto states = make_dephased_states(Mt19937(seed), JumpSpec{q, lanes}, transition_power(q));
+        std::vector<WordSource> sources;
+        for (auto& st : states) {
+            auto lane = std::make_shared<Mt19937>(st);
+            lane->regenerate();
+            sources.push_back([lane] { return lane->next_u32(); });
+        }
+        const StatReport r = lane_cross_correlation(sources, count);
+        *statistic = r.statistic;
+        *p_value = r.p_value;
+        *pass = r.pass ? 1 : 0;
+    });
+}
+
+// monobit (0) / chi2_bytes (1) / lane_cross_correlation of two copies (2) of
+// a constant source (the CLI's --self-test, vmt19937_main.cpp:174-186).
+int vref_stat_constant(std::uint32_t word, std::uint64_t count, int which, double* statistic, double* p_value,
+                       int* pass) {
+    return guarded([&] {
+        WordSource c = [word] { return word; };
+        const StatReport r = which == 0 ? monobit(c, count)
+                             : which == 1 ? chi2_bytes(c, count)
+                                          : lane_cross_correlation({c, c}, count);
+        *statistic = r.statistic;
+        *p_value = r.p_value;
+        *pass = r.pass ? 1 : 0;
+    });
+}
+
 // libstdc++ std::mt19937_64 (the tests' RNG idiom, test_mt19937.cpp:67).
 int vref_mt64(std::uint64_t seed, std::uint64_t count, std::uint64_t* out) {
     std::mt19937_64 g(seed);

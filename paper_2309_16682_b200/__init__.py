@@ -34,7 +34,8 @@ __all__ = [
     "KEFFECTIVE_BITS", "KSTATE_LEN", "MATRIX_DIM", "MATRIX_ROW_WORDS", "jump_matrix", "jump_matrix_pow2",
     "write_jump_matrix_file", "read_jump_matrix_file", "compute_jump_matrix", "jump_matrix_file_name",
     "vec_mat_mul", "jump_state_matrix", "StatReport", "monobit", "chi2_bytes", "stat_counts",
-    "regularized_gamma_q", "K_SIGNIFICANCE",
+    "regularized_gamma_q", "K_SIGNIFICANCE", "lane_cross_correlation", "monobit_from_counts",
+    "chi2_bytes_from_counts",
 ]
 
 KSTATE_LEN = 624
@@ -469,6 +470,26 @@ def monobit(gen: "VmtGenerator", count: int) -> StatReport:
 def chi2_bytes(gen: "VmtGenerator", count: int) -> StatReport:
     """chi2_bytes (stats.cpp:83-107) over the next `count` words of gen."""
     return _report(lib.vmt_chi2_bytes, gen, count)
+
+
+def lane_cross_correlation(gen: "VmtGenerator", count: int) -> StatReport:
+    """lane_cross_correlation (stats.cpp:109-150) over the next count*lanes words."""
+    return _report(lib.vmt_lane_cross_correlation, gen, count)
+
+
+def monobit_from_counts(count: int, ones: int) -> StatReport:
+    r = _capi.StatReportC()
+    check(lib.vmt_monobit_from_counts(count, ones, ctypes.byref(r)))
+    return StatReport(r.name.decode(), r.samples, r.statistic, r.p_value, bool(r.pass_))
+
+
+def chi2_bytes_from_counts(count: int, bins) -> StatReport:
+    b = np.ascontiguousarray(bins, np.uint64)
+    if b.size != 256:
+        raise InvalidArgument(_capi.VMT_EINVAL, "256 byte-value counts expected")
+    r = _capi.StatReportC()
+    check(lib.vmt_chi2_bytes_from_counts(count, b.ctypes.data, ctypes.byref(r)))
+    return StatReport(r.name.decode(), r.samples, r.statistic, r.p_value, bool(r.pass_))
 
 
 def stat_counts(gen: "VmtGenerator", n: int) -> tuple[int, np.ndarray]:

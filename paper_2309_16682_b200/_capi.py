@@ -27,6 +27,7 @@ EXPORTS = [
     "vmt_jump_matrix", "vmt_jump_matrix_pow2", "vmt_write_jump_matrix_file", "vmt_read_jump_matrix_file",
     "vmt_compute_jump_matrix_file", "vmt_vec_mat_mul", "vmt_jump_states_matrix", "vmt_create_from_matrix",
     "vmt_create_from_file", "vmt_stat_counts", "vmt_monobit", "vmt_chi2_bytes", "vmt_regularized_gamma_q",
+    "vmt_monobit_from_counts", "vmt_chi2_bytes_from_counts", "vmt_lane_cross_correlation",
 ]
 
 
@@ -109,6 +110,9 @@ def _load() -> ctypes.CDLL:
         "vmt_monobit": (c.c_int, [H, c.c_uint64, c.POINTER(StatReportC)]),
         "vmt_chi2_bytes": (c.c_int, [H, c.c_uint64, c.POINTER(StatReportC)]),
         "vmt_regularized_gamma_q": (c.c_int, [c.c_double, c.c_double, c.POINTER(c.c_double)]),
+        "vmt_monobit_from_counts": (c.c_int, [c.c_uint64, c.c_uint64, c.POINTER(StatReportC)]),
+        "vmt_chi2_bytes_from_counts": (c.c_int, [c.c_uint64, c.c_void_p, c.POINTER(StatReportC)]),
+        "vmt_lane_cross_correlation": (c.c_int, [H, c.c_uint64, c.POINTER(StatReportC)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -83,11 +83,19 @@ def stats_section(r: RefLib, out: dict) -> None:
             st, pv, ok = r.stat_report(seed, lanes, q, count, which)
             c[name] = {"statistic": st, "p_value": pv, "pass": ok}
         cases.append(c)
+    lc = []
+    for seed, lanes, q, count in ((5489, 4, 20, 1000000), (5489, 16, 16, 100000), (7, 2, 10, 50000)):
+        st, pv, ok = r.lane_corr(seed, lanes, q, count)
+        lc.append({"seed": seed, "lanes": lanes, "q": q, "count": count, "statistic": st, "p_value": pv, "pass": ok})
+    const = []
+    for which, count in ((0, 1000000), (1, 1000000), (2, 62500)):
+        st, pv, ok = r.stat_constant(0xDEADBEEF, count, which)
+        const.append({"which": which, "count": count, "statistic": st, "p_value": pv, "pass": ok})
     gq = []
     for dof in (31, 100, 255, 1023):
         for stat in np.linspace(0.5, 3.0 * dof, 41):
             gq.append([dof / 2.0, float(stat) / 2.0, r.regularized_gamma_q(dof / 2.0, float(stat) / 2.0)])
-    out["stats"] = {"reports": cases, "gamma_q": gq}
+    out["stats"] = {"reports": cases, "gamma_q": gq, "lane_corr": lc, "self_test_0xDEADBEEF": const}
 
 
 def main() -> None:

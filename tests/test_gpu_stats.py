@@ -36,7 +36,7 @@ def test_counts_and_reports_match_reference(golden):
             ref = c[name]
             assert r.name == name and r.samples == c["count"]
             assert r.statistic == ref["statistic"], (name, c["lanes"], r.statistic, ref["statistic"])
-            assert r.p_value == pytest.approx(ref["p_value"], rel=1e-12, abs=1e-300), (name, c["lanes"])
+            assert r.p_value == ref["p_value"], (name, c["lanes"])
             assert r.pass_ == ref["pass"], (name, c["lanes"])
 
 
@@ -85,3 +85,17 @@ def test_large_counts_vs_stored_stream(L):
     assert np.array_equal(bins, tb)
     assert ones == int((tb * POP8).sum())
     assert int(bins.sum()) == 4 * n
+
+
+def test_lane_cross_correlation_matches_reference(golden):
+    """Floating point: the reference's own build mixes vectorised and fused
+    sums, so parity is within 1e-12 relative (statistic and p-value)."""
+    for c in golden["stats"]["lane_corr"]:
+        g = V.VmtGenerator(c["seed"], V.VmtConfig(c["lanes"], jump_exponent=c["q"]))
+        r = V.lane_cross_correlation(g, c["count"])
+        assert r.name == "lane_cross_correlation" and r.samples == c["count"]
+        assert r.statistic == pytest.approx(c["statistic"], rel=1e-12), c
+        assert r.p_value == pytest.approx(c["p_value"], rel=1e-9), c
+        assert r.pass_ == c["pass"]
+    with pytest.raises(V.InvalidArgument):
+        V.lane_cross_correlation(V.VmtGenerator(1, V.VmtConfig(1)), 1000)
