@@ -110,6 +110,31 @@ int vmt_export_state(vmt_handle h, uint32_t* out);
 int vmt_batch_fill_u32(uint32_t seed0, unsigned ngen, unsigned lanes, unsigned jump_exponent,
                        uint64_t n_per_gen, uint32_t* dst, int device, void* stream);
 
+/* A batch of ngen independent generators (seeds seed0..seed0+ngen-1, each a
+ * VmtEngine<lanes> with the same de-phasing; config 3) advancing in lockstep:
+ * vmt_batch_fill writes the next n_per_gen words of every generator,
+ * dst[g*n_per_gen + i] (generator-major), continuing across calls like
+ * next_u32; vmt_batch_skip advances every generator by d words. */
+typedef struct vmt_batch* vmt_batch_handle;
+int vmt_batch_create(uint32_t seed0, unsigned ngen, unsigned lanes, unsigned jump_exponent, int device,
+                     vmt_batch_handle* out);
+int vmt_batch_fill(vmt_batch_handle h, uint32_t* dst, uint64_t n_per_gen, void* stream);
+int vmt_batch_skip(vmt_batch_handle h, uint64_t d);
+uint64_t vmt_batch_position(vmt_batch_handle h);
+/* ngen x 624*lanes interleaved states (VMT_ESTATE off a block boundary). */
+int vmt_batch_export_state(vmt_batch_handle h, uint32_t* out);
+int vmt_batch_destroy(vmt_batch_handle h);
+
+/* Config 4 in one process: the stream's words [0, n) partitioned into ngpus
+ * contiguous ranges (n/ngpus words each, the remainder one word each to the
+ * first devices), each device positioned by one jump, no data exchange.
+ * mode 0 stores into dsts[k] (device k memory), mode 1 only XOR-folds; the
+ * global XOR checksum (bench.cpp:13-18 fold) goes to *checksum when non-NULL
+ * (store mode computes it with a second, fused pass). The multi-process form
+ * (one rank per GPU, torch.distributed) is bench.py / dist.py. */
+int vmt_multi_gpu_fill(uint32_t seed, unsigned lanes, unsigned jump_exponent, uint64_t n, int ngpus,
+                       const int* devices, uint32_t* const* dsts, int mode, uint32_t* checksum);
+
 /* jump_state (jump.cpp:27-33) generalised to arbitrary 64-bit distances, for
  * n boundary states (n x 624 words, lane-major; host or device memory):
  * dst_i = src_i advanced by distances[i] steps (config 5). */

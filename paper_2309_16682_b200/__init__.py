@@ -35,7 +35,7 @@ __all__ = [
     "write_jump_matrix_file", "read_jump_matrix_file", "compute_jump_matrix", "jump_matrix_file_name",
     "vec_mat_mul", "jump_state_matrix", "StatReport", "monobit", "chi2_bytes", "stat_counts",
     "regularized_gamma_q", "K_SIGNIFICANCE", "lane_cross_correlation", "monobit_from_counts",
-    "chi2_bytes_from_counts",
+    "chi2_bytes_from_counts", "VmtBatch", "multi_gpu_fill",
 ]
 
 KSTATE_LEN = 624
@@ -317,6 +317,63 @@ def batch_fill_u32(out, seed0: int, ngen: int, lanes: int, n_per_gen: int,
     q = VMT_FULL_PERIOD if jump_exponent is None else jump_exponent
     check(lib.vmt_batch_fill_u32(seed0, ngen, lanes, q, n_per_gen, addr, device, _stream_for(kind, stream)))
     return out
+
+
+class VmtBatch:
+    """ngen independent generators (seeds seed0.., same lanes and de-phasing)
+    advancing in lockstep (config 3); fill() continues every stream."""
+
+    def __init__(self, seed0: int, ngen: int, lanes: int, jump_exponent: Optional[int] = None, device: int = 0):
+        q = VMT_FULL_PERIOD if jump_exponent is None else jump_exponent
+        self._h = ctypes.c_void_p()
+        check(lib.vmt_batch_create(seed0 & 0xFFFFFFFF, ngen, lanes, q, device, ctypes.byref(self._h)))
+        self.ngen, self.lanes, self.device = ngen, lanes, device
+
+    def close(self) -> None:
+        if self._h:
+            check(lib.vmt_batch_destroy(self._h))
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def position(self) -> int:
+        return int(lib.vmt_batch_position(self._h))
+
+    def fill(self, out, n_per_gen: int, stream=None):
+        _check_dtype(out, np.uint32, "uint32")
+        addr, keep, size, kind = _ptr(out)
+        if size < n_per_gen * self.ngen:
+            raise InvalidArgument(_capi.VMT_EINVAL, "buffer smaller than ngen * n_per_gen")
+        check(lib.vmt_batch_fill(self._h, addr, n_per_gen, _stream_for(kind, stream)))
+        return out
+
+    def skip(self, d: int) -> None:
+        check(lib.vmt_batch_skip(self._h, d))
+
+    def interleaved_states(self) -> np.ndarray:
+        out = np.empty((self.ngen, KSTATE_LEN * self.lanes), np.uint32)
+        check(lib.vmt_batch_export_state(self._h, out.ctypes.data))
+        return out
+
+
+def multi_gpu_fill(seed: int, lanes: int, n: int, devices, outs=None, jump_exponent: Optional[int] = None,
+                   checksum: bool = True) -> Optional[int]:
+    """vmt_multi_gpu_fill: words [0, n) of one stream split over `devices`
+    (store into outs[k] on device k, or XOR only when outs is None)."""
+    q = VMT_FULL_PERIOD if jump_exponent is None else jump_exponent
+    devs = (ctypes.c_int * len(devices))(*devices)
+    ptrs = None
+    if outs is not None:
+        ptrs = (ctypes.c_void_p * len(outs))(*[_ptr(o)[0] for o in outs])
+    x = ctypes.c_uint32()
+    check(lib.vmt_multi_gpu_fill(seed & 0xFFFFFFFF, lanes, q, n, len(devices), devs, ptrs,
+                                 0 if outs is not None else 1, ctypes.byref(x) if checksum else None))
+    return x.value if checksum else None
 
 
 def jump_states(states, distances, out=None, device: int = 0, stream=None):

@@ -28,6 +28,8 @@ EXPORTS = [
     "vmt_compute_jump_matrix_file", "vmt_vec_mat_mul", "vmt_jump_states_matrix", "vmt_create_from_matrix",
     "vmt_create_from_file", "vmt_stat_counts", "vmt_monobit", "vmt_chi2_bytes", "vmt_regularized_gamma_q",
     "vmt_monobit_from_counts", "vmt_chi2_bytes_from_counts", "vmt_lane_cross_correlation",
+    "vmt_batch_create", "vmt_batch_fill", "vmt_batch_skip", "vmt_batch_position", "vmt_batch_export_state",
+    "vmt_batch_destroy", "vmt_multi_gpu_fill",
 ]
 
 
@@ -113,6 +115,14 @@ def _load() -> ctypes.CDLL:
         "vmt_monobit_from_counts": (c.c_int, [c.c_uint64, c.c_uint64, c.POINTER(StatReportC)]),
         "vmt_chi2_bytes_from_counts": (c.c_int, [c.c_uint64, c.c_void_p, c.POINTER(StatReportC)]),
         "vmt_lane_cross_correlation": (c.c_int, [H, c.c_uint64, c.POINTER(StatReportC)]),
+        "vmt_batch_create": (c.c_int, [c.c_uint32, c.c_uint, c.c_uint, c.c_uint, c.c_int, c.POINTER(H)]),
+        "vmt_batch_fill": (c.c_int, [H, c.c_void_p, c.c_uint64, c.c_void_p]),
+        "vmt_batch_skip": (c.c_int, [H, c.c_uint64]),
+        "vmt_batch_position": (c.c_uint64, [H]),
+        "vmt_batch_export_state": (c.c_int, [H, c.c_void_p]),
+        "vmt_batch_destroy": (c.c_int, [H]),
+        "vmt_multi_gpu_fill": (c.c_int, [c.c_uint32, c.c_uint, c.c_uint, c.c_uint64, c.c_int,
+                                         c.POINTER(c.c_int), c.POINTER(c.c_void_p), c.c_int, u32p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -1373,3 +1373,6 @@ int vmt_version(void) { return 100; }
 #include "capi_matrix.inl"
 // Fused statistics consumer: monobit / chi2_bytes counts in MODE_STATS.
 #include "capi_stats.inl"
+
+// Generator batches (config 3) and the single-process multi-GPU fill (config 4).
+#include "capi_batch.inl"

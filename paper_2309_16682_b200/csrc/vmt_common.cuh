@@ -54,7 +54,8 @@ struct GenParams {
     void* out;                         // element of stream word pos_begin (per-chunk offset in batch mode)
     std::uint32_t* xor_partials;       // [gridDim.x] (MODE_XOR)
     unsigned long long* stats_partials; // [gridDim.x][257] (MODE_STATS)
-    std::uint32_t* save_state;         // [624][L] boundary state at save_block (nullable)
+    std::uint32_t* save_state;         // [624][L] boundary state at save_block (nullable); batch
+                                       // mode: [chunk][624][L], one per generator
     unsigned long long first_block;    // absolute block of chunk 0
     unsigned long long end_block;      // exclusive
     unsigned long long pos_begin;      // absolute word range emitted

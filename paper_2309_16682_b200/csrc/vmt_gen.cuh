@@ -420,7 +420,9 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::NT, GenShape<L, R,
     constexpr unsigned long long bw = (unsigned long long)kN * LT;
     constexpr unsigned long long ww = (unsigned long long)W * LT; // stream words per window (all lanes)
     unsigned long long ones = 0; // MODE_STATS
-    const bool save_here = p.save_state != nullptr && (!batch || chunk == 0);
+    // batch mode: every generator (chunk) saves its own boundary state
+    const bool save_here = p.save_state != nullptr;
+    std::uint32_t* const save_dst = p.save_state + (batch ? (unsigned long long)chunk * kN * LT : 0ull);
     int blk_base_slot = 0; // slot of x_{624 r} for the current block r (= 624 r mod RING)
     constexpr int kWins = kN / W;
     // (3 windows x R x V history registers: with V = 4 that spills)
@@ -480,7 +482,7 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::NT, GenShape<L, R,
     };
     for (unsigned long long blk = b_lo; blk < b_hi; ++blk) {
         if (save_here && blk == p.save_block)
-            save_boundary<LT, L, S::RING>(ring, blk_base_slot, p.save_state, col0, tid, S::NT);
+            save_boundary<LT, L, S::RING>(ring, blk_base_slot, save_dst, col0, tid, S::NT);
         if (kHist) {
             // fully unrolled so each window's history registers are static
 #pragma unroll
@@ -497,7 +499,7 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::NT, GenShape<L, R,
     }
     // end-of-range boundary state (block b_hi) when it is the requested one
     if (save_here && b_hi == p.save_block && b_hi == p.end_block)
-        save_boundary<LT, L, S::RING>(ring, blk_base_slot, p.save_state, col0, tid, S::NT);
+        save_boundary<LT, L, S::RING>(ring, blk_base_slot, save_dst, col0, tid, S::NT);
     if (kStaged && tid == 0 && sc.pending)
         bulk_wait_all(); // the staging buffer must outlive the last bulk copy
     if (kFold) {
