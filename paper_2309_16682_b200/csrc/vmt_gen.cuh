@@ -90,11 +90,11 @@ struct GenShape {
     __host__ __device__ static constexpr int stage_bytes() {
         return (TMA && staged_mode<MODE>()) ? W * L * elem_bytes<MODE>() : 0;
     }
-    // MODE_STATS: one 256-bin byte histogram per warp (fewer bank collisions
-    // between warps' shared-memory atomics)
+    // MODE_STATS: one byte-value histogram per lane position, hist[bin][lane]
+    // (32 KB): a warp's 32 atomics always hit 32 different banks
     template <int MODE>
     __host__ __device__ static constexpr int hist_bytes() {
-        return MODE == MODE_STATS ? ((NT + 31) / 32) * 256 * 4 : 0;
+        return MODE == MODE_STATS ? 256 * 32 * 4 : 0;
     }
     template <int MODE>
     __host__ __device__ static constexpr int smem() {
@@ -199,7 +199,7 @@ struct StageCtl {
     unsigned phase;   // mbarrier completions consumed so far
     bool prev_staged; // a bulk copy of buf is outstanding (not yet confirmed read)
     bool pending;     // tid 0's view of the same
-    std::uint32_t* hist; // MODE_STATS: this warp's byte histogram
+    std::uint32_t* hist; // MODE_STATS: this thread's histogram column (stride 32)
 };
 
 // One window of one thread: R new words of V lanes. base: slot of x_p for
@@ -265,17 +265,17 @@ __device__ __forceinline__ void gen_window(std::uint32_t* ring, int base, int a,
             }
         } else if (MODE == MODE_STATS) {
             // acc[0]: one bits of this window's words (folded into 64 bits per
-            // window by the caller); bytes into the warp's histogram
+            // window by the caller); bytes into the hist[bin][lane] columns
 #pragma unroll
             for (int v = 0; v < V; ++v) {
                 const unsigned long long g = g0 + (unsigned long long)i * LT + v;
                 if (FULL || (g >= p.pos_begin && g < p.pos_end)) {
                     const std::uint32_t t = temper(nw[v]);
                     acc[0] += __popc(t);
-                    atomicAdd(sc.hist + (t & 0xFFu), 1u);
-                    atomicAdd(sc.hist + ((t >> 8) & 0xFFu), 1u);
-                    atomicAdd(sc.hist + ((t >> 16) & 0xFFu), 1u);
-                    atomicAdd(sc.hist + (t >> 24), 1u);
+                    atomicAdd(sc.hist + (t & 0xFFu) * 32, 1u);
+                    atomicAdd(sc.hist + ((t >> 8) & 0xFFu) * 32, 1u);
+                    atomicAdd(sc.hist + ((t >> 16) & 0xFFu) * 32, 1u);
+                    atomicAdd(sc.hist + (t >> 24) * 32, 1u);
                 }
             }
         } else if (MODE == MODE_BENCH_TEMPER_XOR) {
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::NT, GenShape<L, R,
     sc.prev_staged = false;
     sc.pending = false;
     sc.hist = reinterpret_cast<std::uint32_t*>(reinterpret_cast<unsigned char*>(ring) + S::RING_BYTES) +
-              (MODE == MODE_STATS ? (tid >> 5) * 256 : 0);
+              (MODE == MODE_STATS ? (tid & 31) : 0);
     // bulk copies need the window's destination 16-byte aligned
     const bool tma_ok =
         kStaged &&
@@ -520,8 +520,8 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::NT, GenShape<L, R,
         unsigned long long* dst = p.stats_partials + (unsigned long long)blockIdx.x * kStatWords;
         for (int b = tid; b < 256; b += S::NT) {
             unsigned long long c = 0;
-            for (int w = 0; w < S::template hist_bytes<MODE>() / 1024; ++w)
-                c += h0[w * 256 + b];
+            for (int l = 0; l < 32; ++l)
+                c += h0[b * 32 + ((l + b) & 31)]; // rotated: the 32 threads of a warp read 32 banks
             dst[1 + b] = c;
         }
         __syncthreads();
