@@ -164,6 +164,20 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows), "source": self.src}
 
 
+def oracle_checksum(total_words, world, args):
+    """The C oracle's XOR of the step's range when tests/golden pins it (N=1:
+    words [0, 2^34) of the config-4 stream; make_golden.py c4_full) -- a
+    committed fixture, not computed here."""
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as f:
+            c = json.load(f)["c4_full"]
+    except Exception:
+        return None
+    if total_words != c["count"] or c["start"] != 0:
+        return None
+    return f"0x{c['xor']:08x}"
+
+
 def measured_peak():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -453,6 +467,7 @@ def main():
                      "kernel": "vmt_gen_kernel", "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_per_launch},
         "checksum_xor": f"0x{csum:08x}",
+        "checksum_oracle": oracle_checksum(T, world, args),
         "clocks": clk,
         "e2e": e2e,
         "e2e_xor": e2e_xor,

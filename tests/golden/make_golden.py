@@ -11,7 +11,7 @@ Sources:
   polynomials x^(2^q) mod P, q = 19932..19936, by plain repeated squaring
   (with the period check x^(2^19937) == x).
 
-Usage: python tests/golden/make_golden.py [--skip-ladder] [--only vmtj|stats]
+Usage: python tests/golden/make_golden.py [--skip-ladder] [--only vmtj|stats|c4_full]
 (--only SECTION recomputes one section into the existing golden.json)
 """
 from __future__ import annotations
@@ -98,6 +98,20 @@ def stats_section(r: RefLib, out: dict) -> None:
     out["stats"] = {"reports": cases, "gamma_q": gq, "lane_corr": lc, "self_test_0xDEADBEEF": const}
 
 
+def c4_full_section(r: RefLib, out: dict) -> None:
+    """The bench workload itself, pinned: XOR checksum of words [0, 2^34) of the
+    config-4 stream (L=32, seed 5489, full-period de-phasing q=19932), by the C
+    oracle (every word regenerated and tempered on the CPU, ~2 min) from lanes
+    de-phased with the period-checked x^(2^19932) fixture."""
+    o = Oracle()
+    polys = dict(np.load(os.path.join(HERE, "xpow2_full.npz")))
+    lanes = o.dephased_states(5489, 32, polys["q19932"])
+    t0 = time.time()
+    x = o.vmt_checksum(lanes, 0, 1 << 34)
+    out["c4_full"] = {"lanes": 32, "seed": 5489, "q": 19932, "start": 0, "count": 1 << 34, "xor": x}
+    print(f"c4 full checksum 0x{x:08x} {time.time() - t0:.1f}s", flush=True)
+
+
 def main() -> None:
     skip_ladder = "--skip-ladder" in sys.argv
     if "--only" in sys.argv:
@@ -105,7 +119,7 @@ def main() -> None:
         path = os.path.join(HERE, "golden.json")
         with open(path) as f:
             out = json.load(f)
-        {"vmtj": vmtj_section, "stats": stats_section}[section](RefLib(), out)
+        {"vmtj": vmtj_section, "stats": stats_section, "c4_full": c4_full_section}[section](RefLib(), out)
         with open(path, "w") as f:
             json.dump(out, f, indent=1)
         return
@@ -184,6 +198,7 @@ def main() -> None:
     print(f"full-period polys {time.time() - t0:.1f}s", flush=True)
     vmtj_section(r, out)
     stats_section(r, out)
+    c4_full_section(r, out)
 
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(out, f, indent=1)

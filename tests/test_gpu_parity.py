@@ -332,3 +332,38 @@ def test_profiling_events_cover_every_fill():
     g.set_profiling(False)
     g.fill_u32(out)
     assert g.profile_totals()[0] == 0
+
+
+def xor_reduce_inplace(t):
+    """XOR of all words of a 1-D uint32 CUDA tensor, by in-place halving."""
+    t = t.view(torch.int32)  # (bitwise ops on uint32 are not implemented for CUDA)
+    n = t.numel()
+    while n > 1:
+        h = n // 2
+        torch.bitwise_xor(t[:h], t[n - h:n], out=t[:h])  # an odd middle word stays at t[h]
+        n = n - h
+    return int(t[0].item()) & 0xFFFFFFFF
+
+
+def test_bench_workload_pinned_to_oracle(golden):
+    """The bench's config-4 step itself (L=32, seed 5489, full period, words
+    [0, 2^34), 64 GiB): the C oracle's XOR of every word (tests/golden,
+    make_golden.py c4_full) equals both the fused checksum and the XOR of the
+    64 GiB actually stored in HBM; words around the 2^32 boundary and at the
+    end equal an independently positioned generator (64-bit indexing)."""
+    c = golden["c4_full"]
+    n = c["count"]
+    g = V.VmtGenerator(c["seed"], V.VmtConfig(c["lanes"]))
+    assert g.jump_exponent() == c["q"]
+    assert g.checksum_xor(n) == c["xor"]
+    out = dev_u32(n)
+    V.VmtGenerator(c["seed"], V.VmtConfig(c["lanes"])).fill_u32(out)
+    for start in ((1 << 32) - 5, n - 1000, (1 << 33) + 12345):
+        h = V.VmtGenerator(c["seed"], V.VmtConfig(c["lanes"]))
+        h.skip(start)
+        w = dev_u32(1000)
+        h.fill_u32(w)
+        m = min(1000, n - start)
+        assert torch.equal(out[start:start + m].view(torch.int32), w[:m].view(torch.int32)), start
+    assert xor_reduce_inplace(out) == c["xor"]
+    del out
