@@ -419,9 +419,9 @@ def main():
 
     # -- end to end into pinned host memory through the public API
     e2e = None
+    out = None  # the 64 GiB device buffer is no longer needed
+    torch.cuda.empty_cache()
     if not args.no_e2e and args.mode == "store":
-        del out
-        torch.cuda.empty_cache()
         try:
             host = torch.empty(count, dtype=torch.uint32, pin_memory=True)
             kind = "pinned"
@@ -444,6 +444,14 @@ def main():
         del host
 
     peak, peak_src = measured_peak()
+    # second denominator: pure-store probes over the same 64 GiB (after the
+    # bench's own buffers are released)
+    store_peaks = {}
+    try:
+        store_peaks = {"grid_stride_gbs": V.store_bandwidth(count * 4, 0, 2, local),
+                       "chunk_per_cta_gbs": V.store_bandwidth(count * 4, 1, 1, local)}
+    except Exception as e:
+        store_peaks = {"error": str(e)}
     bytes_per_launch = count * 4
     achieved = bytes_per_launch / (gen_ms * 1e-3) / 1e9
     traffic = profiled_traffic()
@@ -465,7 +473,9 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": (traffic or {}).get("dram_bytes_per_launch"),
                      "kernel": "vmt_gen_kernel", "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": bytes_per_launch},
+                     "algorithmic_bytes_per_launch": bytes_per_launch,
+                     "store_probe": dict(store_peaks, frac_of_grid_stride=(
+                         achieved / store_peaks["grid_stride_gbs"] if "grid_stride_gbs" in store_peaks else None))},
         "checksum_xor": f"0x{csum:08x}",
         "checksum_oracle": oracle_checksum(T, world, args),
         "clocks": clk,
@@ -484,11 +494,6 @@ def main():
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {e}"}
     if rank == 0 and world == 1 and not args.no_extras:
-        try:
-            del out
-        except NameError:
-            pass
-        torch.cuda.empty_cache()
         try:
             line["other_configs"] = extras(dev)
         except Exception as e:

@@ -256,6 +256,12 @@ int vmt_lane_cross_correlation(vmt_handle h, uint64_t count, vmt_stat_report* ou
 /* detail::regularized_gamma_q (stats.hpp:47-50, stats.cpp:52-60). */
 int vmt_regularized_gamma_q(double a, double x, double* out);
 
+/* Measurement only: GB/s of a pure 16-byte-store kernel over `bytes` of HBM,
+ * pattern 0 = grid-stride, 1 = one contiguous chunk per CTA (the generation
+ * kernel's output pattern); grid = SMs x ctas_per_sm. The second roofline
+ * denominator next to MEASURED_PEAKS.json's copy bandwidth. */
+int vmt_store_bandwidth(int device, uint64_t bytes, int pattern, int ctas_per_sm, double* gbs);
+
 const char* vmt_status_string(int status);
 /* Message of the last failure on this thread. */
 const char* vmt_last_error(void);

@@ -282,7 +282,7 @@ struct Counters {
 void launch_jump_kernel(const JumpParams& jp, cudaStream_t st) {
     int dev = 0;
     VMT_CUDA(cudaGetDevice(&dev));
-    const int slots = device_info(dev).sms * 32;
+    const int slots = device_info(dev).sms * VMT_JUMP_MINB; // resident one-warp jobs
     const int n = jp.njobs;
     // measured on B200 (scratch/jump_bench.cu): split 8 wins below ~1/4 of the
     // warp slots, split 1 from 1/2 upwards
@@ -1348,6 +1348,42 @@ int vmt_stats(vmt_handle h, uint64_t* gen_launches, uint64_t* jump_launches, uin
             *other_launches = h->cnt.other;
         if (lane_jumps)
             *lane_jumps = h->cnt.lane_jumps;
+    });
+}
+
+int vmt_store_bandwidth(int device, uint64_t bytes, int pattern, int ctas_per_sm, double* gbs) {
+    return guarded([&] {
+        require(gbs != nullptr && bytes >= 16, VMT_EINVAL, "bad argument");
+        require(pattern == 0 || pattern == 1, VMT_EINVAL, "pattern must be 0 (grid-stride) or 1 (chunked)");
+        check_device(device);
+        DeviceGuard g(device);
+        const unsigned long long n4 = bytes / 16;
+        DevBuf<uint4> buf;
+        buf.reserve(n4);
+        const int sms = device_info(device).sms;
+        const unsigned grid = (unsigned)(sms * std::max(1, ctas_per_sm));
+        cudaStream_t st = cudaStreamPerThread;
+        auto launch = [&] {
+            if (pattern == 0)
+                vmt_store_probe_stride<<<grid, 512, 0, st>>>(buf.p, n4);
+            else
+                vmt_store_probe_chunked<<<grid, 256, 0, st>>>(buf.p, n4);
+        };
+        launch();
+        VMT_CUDA(cudaGetLastError());
+        cudaEvent_t e0, e1;
+        VMT_CUDA(cudaEventCreate(&e0));
+        VMT_CUDA(cudaEventCreate(&e1));
+        VMT_CUDA(cudaEventRecord(e0, st));
+        for (int r = 0; r < 3; ++r)
+            launch();
+        VMT_CUDA(cudaEventRecord(e1, st));
+        VMT_CUDA(cudaEventSynchronize(e1));
+        float ms = 0;
+        VMT_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        *gbs = double(n4 * 16) * 3 / (ms * 1e-3) / 1e9;
     });
 }
 

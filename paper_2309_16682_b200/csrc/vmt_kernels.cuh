@@ -3,9 +3,11 @@
 //   vmt_gen.cuh     vmt_gen_kernel: twist + temper + emit (the hot path)
 //   vmt_jump.cuh    vmt_jump_kernel (polynomial jump-ahead), seeding, reduction
 //   vmt_matrix.cuh  GF(2) jump matrices: basis states, effective layout, vec_mat_mul
+//   vmt_diag.cuh    pure-store bandwidth probes (measurement only)
 #pragma once
 
 #include "vmt_common.cuh"
 #include "vmt_gen.cuh"
 #include "vmt_jump.cuh"
 #include "vmt_matrix.cuh"
+#include "vmt_diag.cuh"
