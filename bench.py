@@ -343,10 +343,20 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # VMT_BENCH_SHARED_GPU=1: harness test only -- every rank on cuda:0 with
+    # gloo collectives (exercises the N>1 code path on a one-GPU box; its
+    # numbers are not scaling measurements)
+    shared = os.environ.get("VMT_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    coll = torch.device("cpu") if shared else dev  # device of the collectives' tensors
     # T = words the whole job generates per step (all ranks)
     T = args.words * world if args.scaling == "weak" else args.words
     start, count = partition(T, world, rank)
@@ -390,16 +400,16 @@ def main():
     fills, jump_tot, gen_tot = g.profile_totals()
     g.set_profiling(False)
     ms = e0.elapsed_time(e1) / args.steps
-    ms = max_over_ranks(ms, dev)
+    ms = max_over_ranks(ms, coll)
     launches = sum(s1[k] - s0[k] for k in ("gen_launches", "jump_launches", "other_launches"))
     # the generation kernel's own duration and the positioning jumps before
     # it, from the same timed steps
-    gen_ms = max_over_ranks(gen_tot / max(fills, 1), dev)
-    jump_ms = max_over_ranks(jump_tot / max(fills, 1), dev)
+    gen_ms = max_over_ranks(gen_tot / max(fills, 1), coll)
+    jump_ms = max_over_ranks(jump_tot / max(fills, 1), coll)
 
     # -- global checksum of one full 2^34 range (config 4 verification)
     g.seek(start)
-    csum = combine_xor(g.checksum_xor(count), dev)
+    csum = combine_xor(g.checksum_xor(count), coll)
     torch.cuda.synchronize(dev)
 
     # -- end to end, fused consumer: the step's result is the 4-byte XOR
@@ -413,7 +423,7 @@ def main():
     for _ in range(args.steps):
         g.checksum_xor(count)
         g.skip(T - count)
-    xs = max_over_ranks((time.perf_counter() - t0) / args.steps, dev)
+    xs = max_over_ranks((time.perf_counter() - t0) / args.steps, coll)
     e2e_xor = {"value": T / xs, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 4 * world,
                "ms_per_step": xs * 1e3, "mode": "fused XOR checksum, nothing stored"}
 
@@ -438,7 +448,7 @@ def main():
             g.fill_u32(host)
             g.skip(T - count)
         e2e_s = (time.perf_counter() - t0) / args.e2e_steps
-        e2e_s = max_over_ranks(e2e_s, dev)
+        e2e_s = max_over_ranks(e2e_s, coll)
         e2e = {"value": T / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": T * 4,
                "ms_per_step": e2e_s * 1e3, "host_buffer": kind, "steps": args.e2e_steps}
         del host
