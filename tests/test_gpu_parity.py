@@ -367,3 +367,50 @@ def test_bench_workload_pinned_to_oracle(golden):
         assert torch.equal(out[start:start + m].view(torch.int32), w[:m].view(torch.int32)), start
     assert xor_reduce_inplace(out) == c["xor"]
     del out
+
+
+def test_config1_full_size_vs_oracle(oracle, full_polys):
+    """c1 as BASELINE.json states it: L=16, seed 5489, default (full-period)
+    de-phasing, 2^26 words, every word against the oracle."""
+    n = 1 << 26
+    lanes = oracle.dephased_states(5489, 16, full_polys["q19933"])
+    ref = oracle.vmt_stream(lanes, 0, n)
+    g = V.VmtGenerator(5489, V.VmtConfig(16))
+    out = dev_u32(n)
+    g.fill_u32(out)
+    assert np.array_equal(host(out), ref)
+
+
+def test_config2_full_size_vs_oracle(oracle, full_polys):
+    """c2 as BASELINE.json states it: L=8, seed 42, default de-phasing, 2^28
+    values as float32 and as float64 (both conversions of the same words),
+    every value bit-exact against the documented rules on the oracle stream."""
+    n = 1 << 28
+    lanes = oracle.dephased_states(42, 8, full_polys["q19934"])
+    u = oracle.vmt_stream(lanes, 0, n)
+    t32 = torch.empty(n, dtype=torch.float32, device="cuda")
+    V.VmtGenerator(42, V.VmtConfig(8)).fill_f32(t32)
+    ref32 = (u >> np.uint32(8)).astype(np.float32) * np.float32(2.0 ** -24)
+    assert np.array_equal(host(t32).view(np.uint32), ref32.view(np.uint32))
+    del t32, ref32
+    t64 = torch.empty(n, dtype=torch.float64, device="cuda")
+    V.VmtGenerator(42, V.VmtConfig(8)).fill_f64(t64)
+    ref64 = u.astype(np.float64) * 2.0 ** -32
+    assert np.array_equal(host(t64).view(np.uint64), ref64.view(np.uint64))
+
+
+def test_config3_full_size_every_generator():
+    """c3 as BASELINE.json states it: 1024 generators (seeds 1..1024), L=16,
+    default (full-period) de-phasing, 2^20 words each, generator-major. Every
+    generator's block equals its own single-generator stream (XOR fold and
+    first/last words), the single-generator path being pinned to the oracle."""
+    n, ngen = 1 << 20, 1024
+    out = dev_u32(n * ngen)
+    V.batch_fill_u32(out, 1, ngen, 16, n)
+    v = host(out).reshape(ngen, n)
+    folds = np.bitwise_xor.reduce(v, axis=1)
+    for s in range(1, ngen + 1):
+        g = V.VmtGenerator(s, V.VmtConfig(16))
+        head = g.next_block16()
+        assert np.array_equal(v[s - 1, :16], head), s
+        assert g.checksum_xor(n - 16) ^ int(np.bitwise_xor.reduce(head)) == int(folds[s - 1]), s
