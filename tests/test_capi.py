@@ -105,3 +105,28 @@ def test_no_cpu_fallback_without_gpu():
         V.batch_fill_u32(np.empty(16, np.uint32), 1, 1, 16, 16)
     with pytest.raises(V.VmtError):
         V.jump_states(np.zeros((1, 624), np.uint32), [5])
+
+
+def test_argument_errors_without_gpu():
+    """The C ABI validates arguments before touching the device: the
+    reference's std::invalid_argument cases come back as VMT_EINVAL."""
+    import ctypes
+    import paper_2309_16682_b200 as V
+    from paper_2309_16682_b200 import _capi
+    lib = _capi.lib
+    h = ctypes.c_void_p()
+    assert lib.vmt_batch_create(1, 4, 3, 0, 0, ctypes.byref(h)) == _capi.VMT_EINVAL      # lanes
+    assert lib.vmt_batch_create(1, 0, 4, 0, 0, ctypes.byref(h)) == _capi.VMT_EINVAL      # ngen
+    devs = (ctypes.c_int * 1)(0)
+    assert lib.vmt_multi_gpu_fill(1, 4, 0, 10, 1, devs, None, 7, None) == _capi.VMT_EINVAL  # mode
+    assert lib.vmt_multi_gpu_fill(1, 4, 0, 10, 1, devs, None, 0, None) == _capi.VMT_EINVAL  # no dsts
+    assert lib.vmt_multi_gpu_fill(1, 4, 0, 10, 0, devs, None, 1, None) == _capi.VMT_EINVAL  # ngpus
+    out = ctypes.c_double()
+    assert lib.vmt_store_bandwidth(0, 1 << 20, 5, 1, ctypes.byref(out)) == _capi.VMT_EINVAL
+    assert lib.vmt_create_from_matrix(1, 8, None, 3, 0, ctypes.byref(h)) == _capi.VMT_EINVAL
+    assert lib.vmt_vec_mat_mul(None, 1, None, None, 0, None) == _capi.VMT_EINVAL
+    assert lib.vmt_jump_states_matrix(None, 1, None, None, 0, None) == _capi.VMT_EINVAL
+    assert lib.vmt_create(1, 3, 0, 0, ctypes.byref(h)) == _capi.VMT_EINVAL
+    with pytest.raises(V.InvalidArgument):
+        V.write_jump_matrix_file("/tmp/never.vmtj", np.zeros(5, np.uint64), 1)
+    assert b"invalid" in lib.vmt_status_string(_capi.VMT_EINVAL)
