@@ -402,6 +402,7 @@ def main():
     ms = e0.elapsed_time(e1) / args.steps
     ms = max_over_ranks(ms, coll)
     launches = sum(s1[k] - s0[k] for k in ("gen_launches", "jump_launches", "other_launches"))
+    # (the positioning GEMM is cuBLAS's kernel and is not counted)
     # the generation kernel's own duration and the positioning jumps before
     # it, from the same timed steps
     gen_ms = max_over_ranks(gen_tot / max(fills, 1), coll)
@@ -477,9 +478,12 @@ def main():
                    "parallelism": f"stream partition x{world} ({args.scaling})"},
         "gpu_launches": launches,
         "per_gpu_value": count / (ms * 1e-3),
-        "timing_breakdown_ms": {"gen_kernel": gen_ms, "positioning_jumps": jump_ms,
-                                "note": "CUDA events on the fill's stream around the chunk-positioning jump "
-                                        "launch and the generation launch of every timed step"},
+        "timing_breakdown_ms": {"gen_kernel": gen_ms, "positioning": jump_ms,
+                                "positioning_gemms": g.positioning_stats()["gemm_positionings"],
+                                "note": "CUDA events on the fill's stream around the chunk positioning (steady "
+                                        "state: one int8 tensor-core GEMM mapping the previous step's 4736 "
+                                        "chunk lane states forward; first fills: polynomial jumps) and the "
+                                        "generation launch of every timed step"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": (traffic or {}).get("dram_bytes_per_launch"),
                      "kernel": "vmt_gen_kernel", "peak_source": peak_src,

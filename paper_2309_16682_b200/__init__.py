@@ -272,6 +272,15 @@ class VmtGenerator:
     def set_prefetch(self, enable: bool = True) -> None:
         check(lib.vmt_set_prefetch(self._h, int(enable)))
 
+    def set_positioning(self, mode: int = 0) -> None:
+        """0 auto (GEMM for repeating fill shapes), 1 polynomial jumps, 2 GEMM."""
+        check(lib.vmt_set_positioning(self._h, mode))
+
+    def positioning_stats(self) -> dict:
+        g, m = ctypes.c_uint64(), ctypes.c_uint64()
+        check(lib.vmt_positioning_stats(self._h, ctypes.byref(g), ctypes.byref(m)))
+        return {"gemm_positionings": g.value, "cached_matrices": m.value}
+
     def set_profiling(self, enable: bool = True) -> None:
         check(lib.vmt_set_profiling(self._h, int(enable)))
 

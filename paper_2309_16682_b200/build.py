@@ -73,7 +73,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
             errs.append(" ".join(p.args) + "\n" + o)
     if errs:
         raise RuntimeError("nvcc failed:\n" + "\n".join(errs))
-    link = [_nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", LIB + ".tmp", *[o for _, o in jobs], "-lpthread"]
+    cudalib = os.path.join(os.path.dirname(os.path.dirname(os.path.realpath(_nvcc()))), "lib64")
+    link = [_nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", LIB + ".tmp", *[o for _, o in jobs], "-lpthread",
+            "-lcublas", "-Xlinker", "-rpath", "-Xlinker", cudalib]
     if verbose:
         print(" ".join(link), flush=True)
     out = subprocess.run(link, capture_output=True, text=True)

@@ -6,7 +6,6 @@
 
 namespace {
 
-constexpr std::size_t kMatWords = (std::size_t)kDim * kRowWords;
 constexpr std::size_t kMatBytes = kMatWords * 8;
 constexpr std::uint32_t kVmtjVersion = 1;
 constexpr std::size_t kVmtjHeader = 20;

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <list>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -274,7 +275,7 @@ bool is_device_ptr(const void* p) {
 }
 
 struct Counters {
-    std::uint64_t gen = 0, jump = 0, other = 0, lane_jumps = 0;
+    std::uint64_t gen = 0, jump = 0, other = 0, lane_jumps = 0, gemm_positionings = 0;
 };
 
 // One CTA per job; with few jobs several warps split each job's coefficient
@@ -363,6 +364,10 @@ void launch_jumps_affine(cudaStream_t st, const std::uint32_t* src, int src_stri
 
 } // namespace
 
+namespace {
+struct GemmPos; // capi_gemmpos.inl
+}
+
 // ------------------------------------------------------------------ handle --
 struct vmt_generator {
     int device = 0;
@@ -404,6 +409,8 @@ struct vmt_generator {
     cudaEvent_t seg_gen[2] = {nullptr, nullptr}, seg_copy[2] = {nullptr, nullptr};
     unsigned max_chunks = 0;
     int variant = 0;
+    int positioning = 0; // 0 auto, 1 polynomial jumps only, 2 GEMM whenever the fill shape repeats
+    GemmPos* gemm = nullptr;
     Counters cnt;
     bool profile = false;
     // profiling: one event triplet per fill (before jumps, before gen, after
@@ -530,6 +537,13 @@ void reposition(vmt_generator* h, std::uint64_t target, cudaStream_t st) {
     h->cur_block = target;
 }
 
+void matrix_from_poly(const Poly& p, std::uint64_t* rows_dev, cudaStream_t st, Counters& cnt); // capi_matrix.inl
+constexpr std::size_t kMatWords = (std::size_t)kDim * kRowWords;
+
+} // namespace
+#include "capi_gemmpos.inl"
+namespace {
+
 // Profiling event pool (vmt_set_profiling).
 constexpr std::size_t kProfPool = 1024;
 
@@ -640,15 +654,38 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     const std::uint64_t B = (nb + C - 1) / C;
     C = (nb + B - 1) / B;
 
-    // -- chunk start states: prefetched during the previous fill, or jumped now
+    // -- chunk start states: prefetched during the previous fill, by one GEMM
+    // from the previous fill's chunks (same shape, repeating block delta), or
+    // by polynomial jumps from cur
     const bool use_pref = h->pref_valid && h->pref_b0 == b0 && h->pref_B == B && h->pref_C == C;
     h->pref_valid = false;
+    bool positioned = false;
     if (use_pref) {
         // chunk 0 is the prefetched state at b0, so cur needs no re-positioning
         // (the generation kernel saves the next one)
         VMT_CUDA(cudaStreamWaitEvent(st, h->ev_pref, 0));
         h->chunks.swap(h->chunks_alt);
-    } else {
+        positioned = true;
+    }
+    if (!positioned && h->positioning != 1 && C * h->L >= kGemmMinRows) {
+        if (!h->gemm)
+            h->gemm = new GemmPos();
+        GemmPos& gp = *h->gemm;
+        if (gp.last_valid && gp.last_B == B && gp.last_C == C && b0 > gp.last_b0) {
+            const std::uint64_t delta = b0 - gp.last_b0;
+            if (gp.seen.size() > 64)
+                gp.seen.clear();
+            const int seen = ++gp.seen[delta];
+            // build the 400 MB matrix only for a delta that repeats
+            if (gp.mats.count(delta) || seen >= 2 || h->positioning == 2) {
+                h->chunks_alt.reserve((size_t)C * kN * h->L);
+                gemm_position(h, gp, h->chunks.p, h->chunks_alt.p, C * h->L, delta, st);
+                h->chunks.swap(h->chunks_alt);
+                positioned = true;
+            }
+        }
+    }
+    if (!positioned) {
         reposition(h, b0, st);
         h->chunks.reserve((size_t)C * kN * h->L);
         VMT_CUDA(cudaMemcpyAsync(h->chunks.p, h->cur.p, (size_t)kN * h->L * 4, cudaMemcpyDeviceToDevice, st));
@@ -664,6 +701,12 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
             a.p_a = 1;
             launch_jumps_affine(st, h->cur.p, (int)h->L, h->chunks.p, (int)h->L, dp, a, h->cnt);
         }
+    }
+    if (h->gemm) { // h->chunks now holds this fill's chunk starts
+        h->gemm->last_valid = true;
+        h->gemm->last_b0 = b0;
+        h->gemm->last_B = B;
+        h->gemm->last_C = C;
     }
     // -- predict the next fill (same size, same gap) and position its chunks
     // on the side stream while this fill's generation kernel runs: chunk c of
@@ -953,6 +996,7 @@ int vmt_destroy(vmt_handle h) {
             for (auto& t : h->evpool)
                 for (auto& e : t)
                     cudaEventDestroy(e);
+            delete h->gemm;
             if (h->side) {
                 cudaStreamSynchronize(h->side);
                 cudaStreamDestroy(h->side);
@@ -1295,6 +1339,24 @@ int vmt_set_prefetch(vmt_handle h, int enable) {
         require(h != nullptr, VMT_EINVAL, "null handle");
         h->prefetch = enable != 0;
         h->pref_valid = false;
+    });
+}
+
+int vmt_set_positioning(vmt_handle h, int mode) {
+    return guarded([&] {
+        require(h != nullptr, VMT_EINVAL, "null handle");
+        require(mode >= 0 && mode <= 2, VMT_EINVAL, "positioning mode must be 0 (auto), 1 (jumps) or 2 (gemm)");
+        h->positioning = mode;
+    });
+}
+
+int vmt_positioning_stats(vmt_handle h, uint64_t* gemm_positionings, uint64_t* cached_matrices) {
+    return guarded([&] {
+        require(h != nullptr, VMT_EINVAL, "null handle");
+        if (gemm_positionings)
+            *gemm_positionings = h->cnt.gemm_positionings;
+        if (cached_matrices)
+            *cached_matrices = h->gemm ? h->gemm->mats.size() : 0;
     });
 }
 

@@ -141,3 +141,78 @@ __global__ void __launch_bounds__(kVmThreads) vmt_vec_mat_kernel(const std::uint
 }
 
 } // namespace vmt_b200
+
+// ---------------------------------------------------------------------------
+// Chunk positioning as one integer GEMM on the tensor cores (capi_gemmpos.inl).
+// Word-bit coordinates: column 32k + b = bit b of state word k (word 0 holds
+// only its live bit 31: columns 0..30 are always zero), 624*32 = 19968
+// columns. In these coordinates the jump F^d is a 19968 x 19968 0/1 matrix;
+// new_states = old_states * F^d over the integers, mod 2.
+namespace vmt_b200 {
+
+constexpr int kWB = kN * 32; // 19968 word-bit columns
+
+// effective index e <-> word-bit column: e = 0 <-> 31, e >= 1 <-> e + 31
+__device__ __forceinline__ int wb_to_eff(int c) { return c == 31 ? 0 : (c >= 32 ? c - 31 : -1); }
+
+// mwt[j][i] = 1 when input column i contributes to output column j of F^d,
+// from the 19937 effective rows of F^d (row e_in, bit e_out).
+__global__ void vmt_gemm_matrix_kernel(const std::uint64_t* __restrict__ rows, std::int8_t* __restrict__ mwt) {
+    const int ic = blockIdx.x * blockDim.x + threadIdx.x;
+    const int jc = blockIdx.y;
+    if (ic >= kWB)
+        return;
+    const int i = wb_to_eff(ic), j = wb_to_eff(jc);
+    std::int8_t v = 0;
+    if (i >= 0 && j >= 0)
+        v = (std::int8_t)((rows[(long long)i * kRowWords + (j >> 6)] >> (j & 63)) & 1ull);
+    mwt[(long long)jc * kWB + ic] = v;
+}
+
+// a[r][32k + b] = bit b of word k of state r; states interleaved [c][624][L],
+// r = c*L + t, one thread per state word (coalesced reads, 32-byte writes).
+__global__ void vmt_states_to_i8_kernel(const std::uint32_t* __restrict__ st, int L, long long nwords,
+                                        std::int8_t* __restrict__ a) {
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= nwords)
+        return;
+    const int t = (int)(idx % L);
+    const long long ck = idx / L;
+    const int k = (int)(ck % kN);
+    const long long r = (ck / kN) * L + t;
+    std::uint32_t w = st[idx];
+    if (k == 0)
+        w &= kUpperMask;
+    std::uint32_t q[8];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+        const std::uint32_t nib = (w >> (4 * n)) & 15u;
+        q[n] = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+    }
+    uint4* dst = reinterpret_cast<uint4*>(a + r * kWB + 32 * k);
+    dst[0] = make_uint4(q[0], q[1], q[2], q[3]);
+    dst[1] = make_uint4(q[4], q[5], q[6], q[7]);
+}
+
+// new word k of state r = sum_b (prod[r][32k + b] & 1) << b (word 0: its live bit)
+__global__ void vmt_i32_to_states_kernel(const std::int32_t* __restrict__ prod, int L, long long nwords,
+                                         std::uint32_t* __restrict__ st) {
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= nwords)
+        return;
+    const int t = (int)(idx % L);
+    const long long ck = idx / L;
+    const int k = (int)(ck % kN);
+    const long long r = (ck / kN) * L + t;
+    const int4* src = reinterpret_cast<const int4*>(prod + r * kWB + 32 * k);
+    std::uint32_t w = 0;
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+        const int4 v = src[n];
+        w |= ((std::uint32_t)v.x & 1u) << (4 * n) | ((std::uint32_t)v.y & 1u) << (4 * n + 1) |
+             ((std::uint32_t)v.z & 1u) << (4 * n + 2) | ((std::uint32_t)v.w & 1u) << (4 * n + 3);
+    }
+    st[idx] = k == 0 ? (w & kUpperMask) : w;
+}
+
+} // namespace vmt_b200

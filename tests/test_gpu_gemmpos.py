@@ -1,0 +1,66 @@
+"""Steady-state chunk positioning by one int8 tensor-core GEMM (capi_gemmpos.inl):
+the chunk states it produces must make every fill word-identical to the
+polynomial-jump positioning (itself pinned to the oracle)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2309_16682_b200 as V  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need a CUDA device")
+
+
+def i32(t):
+    return t.view(torch.int32)
+
+
+@pytest.mark.parametrize("L,n,gap", [(32, (1 << 26) + 777, 0), (16, 1 << 27, 0), (32, 1 << 25, 12345)])
+def test_gemm_positioning_matches_polynomial_jumps(L, n, gap):
+    ref = V.VmtGenerator(5489, V.VmtConfig(L))
+    ref.set_tuning(max_chunks=148)
+    ref.set_positioning(1)
+    gem = V.VmtGenerator(5489, V.VmtConfig(L))
+    gem.set_tuning(max_chunks=148)
+    gem.set_positioning(0)
+    a = torch.empty(n, dtype=torch.uint32, device="cuda")
+    b = torch.empty(n, dtype=torch.uint32, device="cuda")
+    for i in range(6):
+        ref.fill_u32(a)
+        gem.fill_u32(b)
+        torch.cuda.synchronize()
+        assert torch.equal(i32(a), i32(b)), (L, n, i)
+        ref.skip(gap)
+        gem.skip(gap)
+    st = gem.positioning_stats()
+    assert st["gemm_positionings"] >= 2 and st["cached_matrices"] >= 1
+    assert ref.positioning_stats()["gemm_positionings"] == 0
+
+
+def test_gemm_positioning_mode2_and_shape_changes():
+    """Mode 2 uses the GEMM from the second fill; a different fill size or a
+    backward seek falls back to the jumps; results stay identical."""
+    n = 1 << 25
+    ref = V.VmtGenerator(77, V.VmtConfig(32))
+    gem = V.VmtGenerator(77, V.VmtConfig(32))
+    for g in (ref, gem):
+        g.set_tuning(max_chunks=148)
+    ref.set_positioning(1)
+    gem.set_positioning(2)
+    plan = [n, n, n, n // 2, n, n]
+    for i, m in enumerate(plan):
+        a = torch.empty(m, dtype=torch.uint32, device="cuda")
+        b = torch.empty(m, dtype=torch.uint32, device="cuda")
+        if i == 4:
+            ref.seek(1000)
+            gem.seek(1000)
+        ref.fill_u32(a)
+        gem.fill_u32(b)
+        torch.cuda.synchronize()
+        assert torch.equal(i32(a), i32(b)), i
+    assert gem.positioning_stats()["gemm_positionings"] >= 2
