@@ -83,9 +83,10 @@ void gemm_position(vmt_generator* h, GemmPos& gp, const std::uint32_t* src, std:
     const unsigned grid = (unsigned)((nwords + 255) / 256);
     vmt_states_to_i8_kernel<<<grid, 256, 0, st>>>(src, (int)h->L, nwords, gp.a.p);
     VMT_CUDA(cudaGetLastError());
-    // column-major view: prod^T (19968 x rows) = mat (stored as [out][in]) ^T-op ... i.e.
-    // C(m = 19968, n = rows) = A^T(m x k) B(k x n) with A = mat ([j][i], lda = k),
-    // B = the state bits ([r][i], ldb = k), C = prod ([r][j], ldc = m)
+    // In cuBLAS's column-major terms: C (m = 19968 output bits, n = rows) =
+    // A^T (m x k) * B (k x n) with A = mat stored [out j][in i] (lda = k),
+    // B = the state bits stored [row r][in i] (ldb = k), C = prod stored
+    // [row r][out j] (ldc = m): prod[r][j] = sum_i bits[r][i] * M[i][j].
     const std::int32_t one = 1, zero = 0;
     VMT_CUBLAS(cublasGemmEx(gp.blas, CUBLAS_OP_T, CUBLAS_OP_N, kWB, (int)rows, kWB, &one, mat, CUDA_R_8I, kWB,
                             gp.a.p, CUDA_R_8I, kWB, &zero, gp.prod.p, CUDA_R_32I, kWB, CUBLAS_COMPUTE_32I,
