@@ -481,8 +481,8 @@ def main():
         "timing_breakdown_ms": {"gen_kernel": gen_ms, "positioning": jump_ms,
                                 "positioning_gemms": g.positioning_stats()["gemm_positionings"],
                                 "note": "CUDA events on the fill's stream around the chunk positioning (steady "
-                                        "state: one int8 tensor-core GEMM mapping the previous step's 4736 "
-                                        "chunk lane states forward; first fills: polynomial jumps) and the "
+                                        "state: one FP4 tensor-core GEMM (int8 fallback) mapping the previous "
+                                        "step's 4736 chunk lane states forward; first fills: polynomial jumps) and the "
                                         "generation launch of every timed step"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": (traffic or {}).get("dram_bytes_per_launch"),

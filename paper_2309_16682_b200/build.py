@@ -75,7 +75,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed:\n" + "\n".join(errs))
     cudalib = os.path.join(os.path.dirname(os.path.dirname(os.path.realpath(_nvcc()))), "lib64")
     link = [_nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", LIB + ".tmp", *[o for _, o in jobs], "-lpthread",
-            "-lcublas", "-Xlinker", "-rpath", "-Xlinker", cudalib]
+            "-lcublas", "-lcublasLt", "-Xlinker", "-rpath", "-Xlinker", cudalib]
     if verbose:
         print(" ".join(link), flush=True)
     out = subprocess.run(link, capture_output=True, text=True)

@@ -6,11 +6,13 @@
 // matrix F^(624 D) for all C*L lane states. Instead of C*L polynomial jumps
 // (~0.39 us of GPU each), the new states are one integer GEMM
 //   new[C*L][19968] = old[C*L][19968] x F^(624 D)[19968][19968]  (mod 2)
-// in word-bit coordinates (vmt_matrix.cuh), int8 x int8 -> int32 on the
-// tensor cores via cuBLAS (a plain library GEMM), then packed back into
-// words. The 400 MB int8 matrix for a delta is built once (19937 basis jumps
+// in word-bit coordinates (vmt_matrix.cuh), on the tensor cores via cuBLAS(Lt)
+// (a plain library GEMM): FP4 e2m1 x FP4 with unit NVFP4 block scales and
+// fp32 accumulation (exact: 0/1 inputs, sums <= 19937) where cuBLASLt offers
+// it, else int8 x int8 -> int32; then packed back into words. The 400 MB int8 matrix for a delta is built once (19937 basis jumps
 // + expansion) when the delta repeats; two deltas are cached (a fill size
 // that is not a multiple of the block alternates between two).
+#include <cublasLt.h>
 #include <cublas_v2.h>
 
 namespace {
@@ -20,6 +22,11 @@ constexpr std::size_t kGemmMatBytes = (std::size_t)kWB * kWB;
 
 struct GemmPos {
     cublasHandle_t blas = nullptr;
+    cublasLtHandle_t lt = nullptr;
+    int fp4 = -1; // -1 untried, 0 unavailable (int8 path), 1 in use
+    DevBuf<std::uint8_t> scale_a, scale_b; // unit e4m3 block scales
+    DevBuf<std::uint8_t> work;
+    std::uint64_t scale_rows = 0;
     std::map<std::uint64_t, std::unique_ptr<DevBuf<std::int8_t>>> mats; // delta -> F^(624 delta), word-bit
     std::map<std::uint64_t, int> seen;                                   // delta -> transitions observed
     std::list<std::uint64_t> lru;
@@ -30,6 +37,8 @@ struct GemmPos {
     ~GemmPos() {
         if (blas)
             cublasDestroy(blas);
+        if (lt)
+            cublasLtDestroy(lt);
     }
 };
 
@@ -39,6 +48,70 @@ struct GemmPos {
         if (s_ != CUBLAS_STATUS_SUCCESS)                                                              \
             throw VmtError(VMT_ECUDA, std::string(#x) + ": cuBLAS status " + std::to_string((int)s_));  \
     } while (0)
+
+// D[r][j] (fp32) = sum_i bits[r][i] * M[i][j] with FP4 operands; false when
+// cuBLASLt has no FP4 kernel for the shape (caller falls back to int8).
+bool lt_fp4_gemm(GemmPos& gp, const void* mat, const void* bits, float* prod, std::uint64_t rows, cudaStream_t st) {
+    if (!gp.lt && cublasLtCreate(&gp.lt) != CUBLAS_STATUS_SUCCESS)
+        return false;
+    const std::uint64_t kk = kWB, mm = kWB, nn = rows;
+    // unit scales, one e4m3 byte per 16 elements (swizzled layout is irrelevant
+    // when every scale is 1.0): A covers mm x kk, B covers nn x kk
+    if (gp.scale_rows < rows) {
+        gp.scale_a.reserve(mm * (kk / 16));
+        gp.scale_b.reserve(nn * (kk / 16));
+        VMT_CUDA(cudaMemsetAsync(gp.scale_a.p, 0x38, mm * (kk / 16), st));
+        VMT_CUDA(cudaMemsetAsync(gp.scale_b.p, 0x38, nn * (kk / 16), st));
+        gp.scale_rows = rows;
+    }
+    cublasLtMatmulDesc_t op = nullptr;
+    cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
+    cublasLtMatmulPreference_t pref = nullptr;
+    bool ok = false;
+    do {
+        if (cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32F, CUDA_R_32F) != CUBLAS_STATUS_SUCCESS)
+            break;
+        const cublasOperation_t ta = CUBLAS_OP_T, tb = CUBLAS_OP_N;
+        const cublasLtMatmulMatrixScale_t sm = CUBLASLT_MATMUL_MATRIX_SCALE_VEC16_UE4M3;
+        const void* spa = gp.scale_a.p;
+        const void* spb = gp.scale_b.p;
+        cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &ta, sizeof(ta));
+        cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &tb, sizeof(tb));
+        cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_A_SCALE_MODE, &sm, sizeof(sm));
+        cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_B_SCALE_MODE, &sm, sizeof(sm));
+        cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_A_SCALE_POINTER, &spa, sizeof(spa));
+        cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_B_SCALE_POINTER, &spb, sizeof(spb));
+        if (cublasLtMatrixLayoutCreate(&la, CUDA_R_4F_E2M1, kk, mm, kk) != CUBLAS_STATUS_SUCCESS ||
+            cublasLtMatrixLayoutCreate(&lb, CUDA_R_4F_E2M1, kk, nn, kk) != CUBLAS_STATUS_SUCCESS ||
+            cublasLtMatrixLayoutCreate(&lc, CUDA_R_32F, mm, nn, mm) != CUBLAS_STATUS_SUCCESS)
+            break;
+        const std::size_t ws = 64ull << 20;
+        gp.work.reserve(ws);
+        if (cublasLtMatmulPreferenceCreate(&pref) != CUBLAS_STATUS_SUCCESS)
+            break;
+        cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &ws, sizeof(ws));
+        cublasLtMatmulHeuristicResult_t heur{};
+        int found = 0;
+        if (cublasLtMatmulAlgoGetHeuristic(gp.lt, op, la, lb, lc, lc, pref, 1, &heur, &found) !=
+                CUBLAS_STATUS_SUCCESS ||
+            found == 0)
+            break;
+        const float one = 1.f, zero = 0.f;
+        ok = cublasLtMatmul(gp.lt, op, &one, mat, la, bits, lb, &zero, prod, lc, prod, lc, &heur.algo, gp.work.p, ws,
+                            st) == CUBLAS_STATUS_SUCCESS;
+    } while (false);
+    if (pref)
+        cublasLtMatmulPreferenceDestroy(pref);
+    if (la)
+        cublasLtMatrixLayoutDestroy(la);
+    if (lb)
+        cublasLtMatrixLayoutDestroy(lb);
+    if (lc)
+        cublasLtMatrixLayoutDestroy(lc);
+    if (op)
+        cublasLtMatmulDescDestroy(op);
+    return ok;
+}
 
 const std::int8_t* gemm_matrix(vmt_generator* h, GemmPos& gp, std::uint64_t delta, cudaStream_t st) {
     auto it = gp.mats.find(delta);
@@ -59,8 +132,14 @@ const std::int8_t* gemm_matrix(vmt_generator* h, GemmPos& gp, std::uint64_t delt
     Counters cnt;
     matrix_from_poly(F.x_pow128((std::uint64_t)d, (std::uint64_t)(d >> 64)), rows.p, st, cnt);
     std::unique_ptr<DevBuf<std::int8_t>> m(new DevBuf<std::int8_t>());
-    m->reserve(kGemmMatBytes);
-    vmt_gemm_matrix_kernel<<<dim3((kWB + 255) / 256, kWB), 256, 0, st>>>(rows.p, m->p);
+    if (gp.fp4 == 1) {
+        m->reserve(kGemmMatBytes / 2);
+        vmt_gemm_matrix_fp4_kernel<<<dim3((kWB / 2 + 255) / 256, kWB), 256, 0, st>>>(
+            rows.p, reinterpret_cast<std::uint8_t*>(m->p));
+    } else {
+        m->reserve(kGemmMatBytes);
+        vmt_gemm_matrix_kernel<<<dim3((kWB + 255) / 256, kWB), 256, 0, st>>>(rows.p, m->p);
+    }
     VMT_CUDA(cudaGetLastError());
     VMT_CUDA(cudaStreamSynchronize(st)); // rows is released on return
     h->cnt.other += 1;
@@ -73,6 +152,40 @@ const std::int8_t* gemm_matrix(vmt_generator* h, GemmPos& gp, std::uint64_t delt
 // dst[C][624][L] = src[C][624][L] jumped by 624*delta words, by one GEMM.
 void gemm_position(vmt_generator* h, GemmPos& gp, const std::uint32_t* src, std::uint32_t* dst, std::uint64_t rows,
                    std::uint64_t delta, cudaStream_t st) {
+    static const bool no_fp4 = std::getenv("VMT_GEMM_INT8") != nullptr;
+    if (gp.fp4 < 0 && no_fp4)
+        gp.fp4 = 0;
+    if (gp.fp4 != 0) {
+        // FP4 path (probe on first use; a failure switches to int8 for good)
+        if (gp.fp4 < 0)
+            gp.fp4 = 1;
+        const std::int8_t* mat = gemm_matrix(h, gp, delta, st);
+        const long long nwords = (long long)rows * kN;
+        const unsigned grid = (unsigned)((nwords + 255) / 256);
+        // the block-scale layout tiles rows by 128: pad the state operand with
+        // zero rows to a multiple of 128
+        const std::uint64_t rows_pad = (rows + 127) / 128 * 128;
+        gp.a.reserve(rows_pad * kWB / 2);
+        gp.prod.reserve(rows_pad * kWB);
+        if (rows_pad > rows)
+            VMT_CUDA(cudaMemsetAsync(gp.a.p + rows * kWB / 2, 0, (rows_pad - rows) * kWB / 2, st));
+        vmt_states_to_fp4_kernel<<<grid, 256, 0, st>>>(src, (int)h->L, nwords,
+                                                        reinterpret_cast<std::uint8_t*>(gp.a.p));
+        VMT_CUDA(cudaGetLastError());
+        float* prod = reinterpret_cast<float*>(gp.prod.p);
+        if (lt_fp4_gemm(gp, mat, gp.a.p, prod, rows_pad, st)) {
+            vmt_f32_to_states_kernel<<<grid, 256, 0, st>>>(prod, (int)h->L, nwords, dst);
+            VMT_CUDA(cudaGetLastError());
+            h->cnt.other += 2; // expand + pack (the GEMM itself is cuBLASLt's kernel)
+            h->cnt.gemm_positionings += 1;
+            return;
+        }
+        // no FP4 kernel: drop the FP4 matrices and use int8 from now on
+        VMT_CUDA(cudaStreamSynchronize(st));
+        gp.fp4 = 0;
+        gp.mats.clear();
+        gp.lru.clear();
+    }
     const std::int8_t* mat = gemm_matrix(h, gp, delta, st);
     if (!gp.blas)
         VMT_CUBLAS(cublasCreate(&gp.blas));

@@ -216,3 +216,73 @@ __global__ void vmt_i32_to_states_kernel(const std::int32_t* __restrict__ prod, 
 }
 
 } // namespace vmt_b200
+
+// FP4 (e2m1) variants of the GEMM positioning operands: 1.0 = code 0x2, two
+// values per byte, low nibble first; unit block scales make the product exact
+// (0/1 inputs, fp32 accumulation of at most 19937 ones).
+namespace vmt_b200 {
+
+__global__ void vmt_gemm_matrix_fp4_kernel(const std::uint64_t* __restrict__ rows, std::uint8_t* __restrict__ mwt) {
+    const int ip2 = blockIdx.x * blockDim.x + threadIdx.x; // column pair
+    const int jc = blockIdx.y;
+    if (2 * ip2 >= kWB)
+        return;
+    const int j = wb_to_eff(jc);
+    std::uint8_t v = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int i = wb_to_eff(2 * ip2 + h);
+        if (i >= 0 && j >= 0 && ((rows[(long long)i * kRowWords + (j >> 6)] >> (j & 63)) & 1ull))
+            v |= (std::uint8_t)(0x2u << (4 * h));
+    }
+    mwt[(long long)jc * (kWB / 2) + ip2] = v;
+}
+
+__global__ void vmt_states_to_fp4_kernel(const std::uint32_t* __restrict__ st, int L, long long nwords,
+                                         std::uint8_t* __restrict__ a) {
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= nwords)
+        return;
+    const int t = (int)(idx % L);
+    const long long ck = idx / L;
+    const int k = (int)(ck % kN);
+    const long long r = (ck / kN) * L + t;
+    std::uint32_t w = st[idx];
+    if (k == 0)
+        w &= kUpperMask;
+    // byte n holds bits 2n (low nibble) and 2n+1 (high nibble) as code 0x2
+    std::uint32_t q[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        std::uint32_t v = 0;
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+            const std::uint32_t b = (w >> (8 * m + 2 * n)) & 3u;
+            v |= (((b & 1u) << 1) | ((b & 2u) << 4)) << (8 * n);
+        }
+        q[m] = v;
+    }
+    *reinterpret_cast<uint4*>(a + r * (kWB / 2) + 16 * k) = make_uint4(q[0], q[1], q[2], q[3]);
+}
+
+__global__ void vmt_f32_to_states_kernel(const float* __restrict__ prod, int L, long long nwords,
+                                         std::uint32_t* __restrict__ st) {
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= nwords)
+        return;
+    const int t = (int)(idx % L);
+    const long long ck = idx / L;
+    const int k = (int)(ck % kN);
+    const long long r = (ck / kN) * L + t;
+    const float4* src = reinterpret_cast<const float4*>(prod + r * kWB + 32 * k);
+    std::uint32_t w = 0;
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+        const float4 v = src[n];
+        w |= ((std::uint32_t)(int)v.x & 1u) << (4 * n) | ((std::uint32_t)(int)v.y & 1u) << (4 * n + 1) |
+             ((std::uint32_t)(int)v.z & 1u) << (4 * n + 2) | ((std::uint32_t)(int)v.w & 1u) << (4 * n + 3);
+    }
+    st[idx] = k == 0 ? (w & kUpperMask) : w;
+}
+
+} // namespace vmt_b200

@@ -64,3 +64,30 @@ def test_gemm_positioning_mode2_and_shape_changes():
         torch.cuda.synchronize()
         assert torch.equal(i32(a), i32(b)), i
     assert gem.positioning_stats()["gemm_positionings"] >= 2
+
+
+def test_int8_backend_matches():
+    """The int8 GEMM backend (used where cuBLASLt has no FP4 kernel; forced
+    here by VMT_GEMM_INT8) gives the same words."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, torch
+sys.path.insert(0, ".")
+import paper_2309_16682_b200 as V
+n = (1 << 25) + 5
+ref = V.VmtGenerator(9, V.VmtConfig(16)); gem = V.VmtGenerator(9, V.VmtConfig(16))
+for g in (ref, gem): g.set_tuning(max_chunks=148)
+ref.set_positioning(1); gem.set_positioning(2)
+a = torch.empty(n, dtype=torch.uint32, device="cuda"); b = torch.empty(n, dtype=torch.uint32, device="cuda")
+for i in range(4):
+    ref.fill_u32(a); gem.fill_u32(b); torch.cuda.synchronize()
+    assert torch.equal(a.view(torch.int32), b.view(torch.int32)), i
+assert gem.positioning_stats()["gemm_positionings"] >= 2
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, VMT_GEMM_INT8="1"))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
