@@ -91,3 +91,29 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
                        env=dict(os.environ, VMT_GEMM_INT8="1"))
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_gemm_positioning_in_fused_modes():
+    """The fused consumers (XOR checksum, statistics) and the float fills go
+    through the same positioning: repeated calls agree with the jump path."""
+    n = (1 << 26) + 3
+    ref = V.VmtGenerator(3, V.VmtConfig(32))
+    gem = V.VmtGenerator(3, V.VmtConfig(32))
+    for g in (ref, gem):
+        g.set_tuning(max_chunks=148)
+    ref.set_positioning(1)
+    gem.set_positioning(2)
+    for _ in range(3):
+        assert ref.checksum_xor(n) == gem.checksum_xor(n)
+    for _ in range(3):
+        o1, b1 = ref.stat_counts(n)
+        o2, b2 = gem.stat_counts(n)
+        assert o1 == o2 and np.array_equal(b1, b2)
+    f1 = torch.empty(n, dtype=torch.float32, device="cuda")
+    f2 = torch.empty(n, dtype=torch.float32, device="cuda")
+    for _ in range(3):
+        ref.fill_f32(f1)
+        gem.fill_f32(f2)
+        torch.cuda.synchronize()
+        assert torch.equal(f1.view(torch.int32), f2.view(torch.int32))
+    assert gem.positioning_stats()["gemm_positionings"] >= 6
