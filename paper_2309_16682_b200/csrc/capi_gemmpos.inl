@@ -15,9 +15,13 @@
 #include <cublasLt.h>
 #include <cublas_v2.h>
 
+#ifndef VMT_GEMM_MIN_ROWS
+#define VMT_GEMM_MIN_ROWS 1024
+#endif
+
 namespace {
 
-constexpr std::uint64_t kGemmMinRows = 2048; // below this the polynomial jumps win
+constexpr std::uint64_t kGemmMinRows = VMT_GEMM_MIN_ROWS; // below this the polynomial jumps win
 constexpr std::size_t kGemmMatBytes = (std::size_t)kWB * kWB;
 
 struct GemmPos {
@@ -28,8 +32,9 @@ struct GemmPos {
     DevBuf<std::uint8_t> work;
     std::uint64_t scale_rows = 0;
     std::map<std::uint64_t, std::unique_ptr<DevBuf<std::int8_t>>> mats; // delta -> F^(624 delta), word-bit
+    std::map<std::uint64_t, std::uint64_t> last_use;                     // delta -> tick of its last use
     std::map<std::uint64_t, int> seen;                                   // delta -> transitions observed
-    std::list<std::uint64_t> lru;
+    std::uint64_t tick = 0;
     DevBuf<std::int8_t> a;
     DevBuf<std::int32_t> prod;
     bool last_valid = false;
@@ -113,17 +118,30 @@ bool lt_fp4_gemm(GemmPos& gp, const void* mat, const void* bits, float* prod, st
     return ok;
 }
 
+// The matrix for a delta, building it when there is room: at most two are
+// cached, and one is only replaced after 32 positionings without a use -- so
+// sizes that wander cannot turn every fill into a 10 ms matrix build.
+// nullptr: no matrix (the caller uses the polynomial jumps).
 const std::int8_t* gemm_matrix(vmt_generator* h, GemmPos& gp, std::uint64_t delta, cudaStream_t st) {
     auto it = gp.mats.find(delta);
     if (it != gp.mats.end()) {
-        gp.lru.remove(delta);
-        gp.lru.push_front(delta);
+        gp.last_use[delta] = gp.tick;
         return it->second->p;
     }
     if (gp.mats.size() >= 2) {
+        std::uint64_t victim = 0;
+        bool found = false;
+        for (auto& kv : gp.mats)
+            if (gp.tick - gp.last_use[kv.first] > 32) {
+                victim = kv.first;
+                found = true;
+                break;
+            }
+        if (!found)
+            return nullptr;
         VMT_CUDA(cudaStreamSynchronize(st));
-        gp.mats.erase(gp.lru.back());
-        gp.lru.pop_back();
+        gp.mats.erase(victim);
+        gp.last_use.erase(victim);
     }
     Gf2Field& F = Gf2Field::instance();
     const unsigned __int128 d = (unsigned __int128)kN * delta;
@@ -145,13 +163,14 @@ const std::int8_t* gemm_matrix(vmt_generator* h, GemmPos& gp, std::uint64_t delt
     h->cnt.other += 1;
     const std::int8_t* p = m->p;
     gp.mats[delta] = std::move(m);
-    gp.lru.push_front(delta);
+    gp.last_use[delta] = gp.tick;
     return p;
 }
 
 // dst[C][624][L] = src[C][624][L] jumped by 624*delta words, by one GEMM.
-void gemm_position(vmt_generator* h, GemmPos& gp, const std::uint32_t* src, std::uint32_t* dst, std::uint64_t rows,
+bool gemm_position(vmt_generator* h, GemmPos& gp, const std::uint32_t* src, std::uint32_t* dst, std::uint64_t rows,
                    std::uint64_t delta, cudaStream_t st) {
+    ++gp.tick;
     static const bool no_fp4 = std::getenv("VMT_GEMM_INT8") != nullptr;
     if (gp.fp4 < 0 && no_fp4)
         gp.fp4 = 0;
@@ -160,6 +179,8 @@ void gemm_position(vmt_generator* h, GemmPos& gp, const std::uint32_t* src, std:
         if (gp.fp4 < 0)
             gp.fp4 = 1;
         const std::int8_t* mat = gemm_matrix(h, gp, delta, st);
+        if (!mat)
+            return false;
         const long long nwords = (long long)rows * kN;
         const unsigned grid = (unsigned)((nwords + 255) / 256);
         // the block-scale layout tiles rows by 128: pad the state operand with
@@ -178,15 +199,17 @@ void gemm_position(vmt_generator* h, GemmPos& gp, const std::uint32_t* src, std:
             VMT_CUDA(cudaGetLastError());
             h->cnt.other += 2; // expand + pack (the GEMM itself is cuBLASLt's kernel)
             h->cnt.gemm_positionings += 1;
-            return;
+            return true;
         }
         // no FP4 kernel: drop the FP4 matrices and use int8 from now on
         VMT_CUDA(cudaStreamSynchronize(st));
         gp.fp4 = 0;
         gp.mats.clear();
-        gp.lru.clear();
+        gp.last_use.clear();
     }
     const std::int8_t* mat = gemm_matrix(h, gp, delta, st);
+    if (!mat)
+        return false;
     if (!gp.blas)
         VMT_CUBLAS(cublasCreate(&gp.blas));
     VMT_CUBLAS(cublasSetStream(gp.blas, st));
@@ -208,6 +231,7 @@ void gemm_position(vmt_generator* h, GemmPos& gp, const std::uint32_t* src, std:
     VMT_CUDA(cudaGetLastError());
     h->cnt.other += 2; // expand + pack (the GEMM itself is cuBLAS's kernel)
     h->cnt.gemm_positionings += 1;
+    return true;
 }
 
 } // namespace

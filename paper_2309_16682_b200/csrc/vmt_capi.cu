@@ -679,9 +679,10 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
             // build the 400 MB matrix only for a delta that repeats
             if (gp.mats.count(delta) || seen >= 2 || h->positioning == 2) {
                 h->chunks_alt.reserve((size_t)C * kN * h->L);
-                gemm_position(h, gp, h->chunks.p, h->chunks_alt.p, C * h->L, delta, st);
-                h->chunks.swap(h->chunks_alt);
-                positioned = true;
+                if (gemm_position(h, gp, h->chunks.p, h->chunks_alt.p, C * h->L, delta, st)) {
+                    h->chunks.swap(h->chunks_alt);
+                    positioned = true;
+                }
             }
         }
     }
