@@ -240,8 +240,11 @@ def extras(dev) -> dict:
 
     stream = torch.cuda.current_stream(dev)
 
-    def timed(fn, reps=3):
-        fn()
+    def timed(fn, reps=3, warm=4):
+        # steady state: the warm calls include the one-time positioning-matrix
+        # build of a repeating fill shape
+        for _ in range(warm):
+            fn()
         torch.cuda.synchronize(dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
