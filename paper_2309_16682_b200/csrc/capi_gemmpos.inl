@@ -21,7 +21,13 @@
 
 namespace {
 
-constexpr std::uint64_t kGemmMinRows = VMT_GEMM_MIN_ROWS; // below this the polynomial jumps win
+// below this many lane states the polynomial jumps win (env VMT_GEMM_MIN_ROWS overrides)
+inline std::uint64_t gemm_min_rows() {
+    static const std::uint64_t v =
+        std::getenv("VMT_GEMM_MIN_ROWS") ? std::strtoull(std::getenv("VMT_GEMM_MIN_ROWS"), nullptr, 10)
+                                         : (std::uint64_t)VMT_GEMM_MIN_ROWS;
+    return v;
+}
 constexpr std::size_t kGemmMatBytes = (std::size_t)kWB * kWB;
 
 struct GemmPos {

@@ -667,7 +667,7 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
         h->chunks.swap(h->chunks_alt);
         positioned = true;
     }
-    if (!positioned && h->positioning != 1 && C * h->L >= kGemmMinRows) {
+    if (!positioned && h->positioning != 1 && C * h->L >= gemm_min_rows()) {
         if (!h->gemm)
             h->gemm = new GemmPos();
         GemmPos& gp = *h->gemm;
