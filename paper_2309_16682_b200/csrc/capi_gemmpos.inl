@@ -174,8 +174,39 @@ const std::int8_t* gemm_matrix(vmt_generator* h, GemmPos& gp, std::uint64_t delt
 }
 
 // dst[C][624][L] = src[C][624][L] jumped by 624*delta words, by one GEMM.
+// A cached matrix usable for `delta`: exact, or a base delta at most 4 blocks
+// below (the rest is regenerated); 0 when there is none.
+std::uint64_t usable_base(const GemmPos& gp, std::uint64_t delta) {
+    std::uint64_t best = 0;
+    for (auto& kv : gp.mats)
+        if (kv.first <= delta && delta - kv.first <= 4 && kv.first > best)
+            best = kv.first;
+    return best;
+}
+
+bool gemm_position_exact(vmt_generator* h, GemmPos& gp, const std::uint32_t* src, std::uint32_t* dst,
+                         std::uint64_t rows, std::uint64_t delta, cudaStream_t st);
+
+// dst = src jumped by 624*delta words: one GEMM with the matrix of delta
+// (built when there is room in the cache), or -- when the cache is full of
+// recently used matrices -- with one of a delta at most 4 blocks below
+// followed by that many blocks of regeneration.
 bool gemm_position(vmt_generator* h, GemmPos& gp, const std::uint32_t* src, std::uint32_t* dst, std::uint64_t rows,
                    std::uint64_t delta, cudaStream_t st) {
+    if (gemm_position_exact(h, gp, src, dst, rows, delta, st))
+        return true;
+    const std::uint64_t base = usable_base(gp, delta);
+    if (base == 0 || !gemm_position_exact(h, gp, src, dst, rows, base, st))
+        return false;
+    vmt_advance_blocks_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(dst, (int)h->L, (long long)rows,
+                                                                             (int)(delta - base));
+    VMT_CUDA(cudaGetLastError());
+    h->cnt.other += 1;
+    return true;
+}
+
+bool gemm_position_exact(vmt_generator* h, GemmPos& gp, const std::uint32_t* src, std::uint32_t* dst,
+                         std::uint64_t rows, std::uint64_t delta, cudaStream_t st) {
     ++gp.tick;
     static const bool no_fp4 = std::getenv("VMT_GEMM_INT8") != nullptr;
     if (gp.fp4 < 0 && no_fp4)

@@ -677,7 +677,7 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
                 gp.seen.clear();
             const int seen = ++gp.seen[delta];
             // build the 400 MB matrix only for a delta that repeats
-            if (gp.mats.count(delta) || seen >= 2 || h->positioning == 2) {
+            if (usable_base(gp, delta) || seen >= 2 || h->positioning == 2) {
                 h->chunks_alt.reserve((size_t)C * kN * h->L);
                 if (gemm_position(h, gp, h->chunks.p, h->chunks_alt.p, C * h->L, delta, st)) {
                     h->chunks.swap(h->chunks_alt);

@@ -272,10 +272,11 @@ __device__ __forceinline__ void gen_window(std::uint32_t* ring, int base, int a,
                 if (FULL || (g >= p.pos_begin && g < p.pos_end)) {
                     const std::uint32_t t = temper(nw[v]);
                     acc[0] += __popc(t);
-                    atomicAdd(sc.hist + (t & 0xFFu) * 32, 1u);
-                    atomicAdd(sc.hist + ((t >> 8) & 0xFFu) * 32, 1u);
-                    atomicAdd(sc.hist + ((t >> 16) & 0xFFu) * 32, 1u);
-                    atomicAdd(sc.hist + (t >> 24) * 32, 1u);
+                    // PRMT extracts a byte zero-extended, one LEA forms the address
+                    atomicAdd(sc.hist + (__byte_perm(t, 0u, 0x4440u) << 5), 1u);
+                    atomicAdd(sc.hist + (__byte_perm(t, 0u, 0x4441u) << 5), 1u);
+                    atomicAdd(sc.hist + (__byte_perm(t, 0u, 0x4442u) << 5), 1u);
+                    atomicAdd(sc.hist + (__byte_perm(t, 0u, 0x4443u) << 5), 1u);
                 }
             }
         } else if (MODE == MODE_BENCH_TEMPER_XOR) {

@@ -286,3 +286,25 @@ __global__ void vmt_f32_to_states_kernel(const float* __restrict__ prod, int L, 
 }
 
 } // namespace vmt_b200
+
+// Advances k whole blocks: every state of an interleaved [C][624][L] array
+// regenerated k times in place (the reference's regenerate,
+// mt19937.cpp:36-49), one thread per lane state. Used to reuse the positioning
+// matrix of a block delta D for deltas D+1..D+4.
+namespace vmt_b200 {
+
+__global__ void vmt_advance_blocks_kernel(std::uint32_t* st, int L, long long nstates, int k) {
+    const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nstates)
+        return;
+    std::uint32_t* x = st + (s / L) * (long long)kN * L + (s % L); // word i at x[i * L]
+    for (int r = 0; r < k; ++r) {
+        for (int i = 0; i < kN; ++i) {
+            const int i1 = i + 1 < kN ? i + 1 : 0;
+            const int im = i + kM < kN ? i + kM : i + kM - kN;
+            x[(long long)i * L] = twist(x[(long long)i * L], x[(long long)i1 * L], x[(long long)im * L]);
+        }
+    }
+}
+
+} // namespace vmt_b200

@@ -20,7 +20,7 @@ def i32(t):
     return t.view(torch.int32)
 
 
-@pytest.mark.parametrize("L,n,gap", [(32, (1 << 26) + 777, 0), (16, 1 << 27, 0), (32, 1 << 25, 12345)])
+@pytest.mark.parametrize("L,n,gap", [(32, (1 << 26) + 777, 0), (16, 1 << 27, 0), (32, 1 << 25, 12345), (8, 1 << 28, 0)])
 def test_gemm_positioning_matches_polynomial_jumps(L, n, gap):
     ref = V.VmtGenerator(5489, V.VmtConfig(L))
     ref.set_tuning(max_chunks=148)
@@ -117,3 +117,26 @@ def test_gemm_positioning_in_fused_modes():
         torch.cuda.synchronize()
         assert torch.equal(f1.view(torch.int32), f2.view(torch.int32))
     assert gem.positioning_stats()["gemm_positionings"] >= 6
+
+
+def test_gemm_positioning_reuses_matrix_with_block_advance():
+    """Three fill sizes cycling (block deltas D, D+1, D+2): two matrices get
+    cached, the third delta reuses the one a block below and regenerates the
+    remaining block (vmt_advance_blocks_kernel); words stay identical."""
+    bw = 624 * 32
+    ref = V.VmtGenerator(11, V.VmtConfig(32))
+    gem = V.VmtGenerator(11, V.VmtConfig(32))
+    for g in (ref, gem):
+        g.set_tuning(max_chunks=148)
+    ref.set_positioning(1)
+    gem.set_positioning(2)
+    for k in range(10):
+        n = bw * (3000 + (k % 3))
+        a = torch.empty(n, dtype=torch.uint32, device="cuda")
+        b = torch.empty(n, dtype=torch.uint32, device="cuda")
+        ref.fill_u32(a)
+        gem.fill_u32(b)
+        torch.cuda.synchronize()
+        assert torch.equal(i32(a), i32(b)), k
+    st = gem.positioning_stats()
+    assert st["cached_matrices"] == 2 and st["gemm_positionings"] >= 7
