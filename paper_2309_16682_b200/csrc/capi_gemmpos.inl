@@ -187,21 +187,25 @@ std::uint64_t usable_base(const GemmPos& gp, std::uint64_t delta) {
 bool gemm_position_exact(vmt_generator* h, GemmPos& gp, const std::uint32_t* src, std::uint32_t* dst,
                          std::uint64_t rows, std::uint64_t delta, cudaStream_t st);
 
-// dst = src jumped by 624*delta words: one GEMM with the matrix of delta
-// (built when there is room in the cache), or -- when the cache is full of
-// recently used matrices -- with one of a delta at most 4 blocks below
-// followed by that many blocks of regeneration.
+// dst = src jumped by 624*delta words: one GEMM with the matrix of a cached
+// base delta B in [delta-4, delta] (the largest, so exact when cached)
+// followed by delta-B blocks of in-place regeneration (microseconds), or with
+// a new matrix built for delta -- a fill size alternating between block
+// deltas D and D+1 then needs one matrix when D repeats first.
 bool gemm_position(vmt_generator* h, GemmPos& gp, const std::uint32_t* src, std::uint32_t* dst, std::uint64_t rows,
                    std::uint64_t delta, cudaStream_t st) {
-    if (gemm_position_exact(h, gp, src, dst, rows, delta, st))
-        return true;
-    const std::uint64_t base = usable_base(gp, delta);
-    if (base == 0 || !gemm_position_exact(h, gp, src, dst, rows, base, st))
+    std::uint64_t base = usable_base(gp, delta);
+    if (base == 0)
+        base = delta;
+    if (!gemm_position_exact(h, gp, src, dst, rows, base, st))
         return false;
-    vmt_advance_blocks_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(dst, (int)h->L, (long long)rows,
-                                                                             (int)(delta - base));
-    VMT_CUDA(cudaGetLastError());
-    h->cnt.other += 1;
+    if (delta > base) {
+        const unsigned grid = (unsigned)((rows + kAdvWarps - 1) / kAdvWarps);
+        vmt_advance_blocks_kernel<<<grid, 32 * kAdvWarps, 0, st>>>(dst, (int)h->L, (long long)rows,
+                                                                  (int)(delta - base));
+        VMT_CUDA(cudaGetLastError());
+        h->cnt.other += 1;
+    }
     return true;
 }
 

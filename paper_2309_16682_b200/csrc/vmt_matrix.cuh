@@ -289,22 +289,57 @@ __global__ void vmt_f32_to_states_kernel(const float* __restrict__ prod, int L, 
 
 // Advances k whole blocks: every state of an interleaved [C][624][L] array
 // regenerated k times in place (the reference's regenerate,
-// mt19937.cpp:36-49), one thread per lane state. Used to reuse the positioning
-// matrix of a block delta D for deltas D+1..D+4.
+// mt19937.cpp:36-49), one warp per lane state in shared memory. The block
+// splits into the recurrence's dependency phases [0,227), [227,454),
+// [454,623), {623}: inside a phase every new word depends only on words the
+// phase does not write, so each phase is computed into registers and written
+// after a __syncwarp. Used to reuse the positioning matrix of a block delta D
+// for deltas D+1..D+4.
 namespace vmt_b200 {
 
-__global__ void vmt_advance_blocks_kernel(std::uint32_t* st, int L, long long nstates, int k) {
-    const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+constexpr int kAdvWarps = 4;
+
+__global__ void __launch_bounds__(32 * kAdvWarps) vmt_advance_blocks_kernel(std::uint32_t* st, int L,
+                                                                           long long nstates, int k) {
+    __shared__ std::uint32_t xs[kAdvWarps][kN];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long long s = (long long)blockIdx.x * kAdvWarps + w;
     if (s >= nstates)
         return;
-    std::uint32_t* x = st + (s / L) * (long long)kN * L + (s % L); // word i at x[i * L]
+    std::uint32_t* x = xs[w];
+    std::uint32_t* g = st + (s / L) * (long long)kN * L + (s % L); // word i at g[i * L]
+    for (int i = lane; i < kN; i += 32)
+        x[i] = g[(long long)i * L];
+    __syncwarp();
     for (int r = 0; r < k; ++r) {
-        for (int i = 0; i < kN; ++i) {
-            const int i1 = i + 1 < kN ? i + 1 : 0;
-            const int im = i + kM < kN ? i + kM : i + kM - kN;
-            x[(long long)i * L] = twist(x[(long long)i * L], x[(long long)i1 * L], x[(long long)im * L]);
+        // phases [0,227), [227,454), [454,623): x[i] = twist(x[i], x[i+1], x[i+397 mod 624])
+#pragma unroll 1
+        for (int ph = 0; ph < 3; ++ph) {
+            const int lo = ph * 227, hi = ph == 2 ? kN - 1 : lo + 227;
+            std::uint32_t y[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int i = lo + lane + 32 * j;
+                if (i < hi) {
+                    const int im = i + kM < kN ? i + kM : i + kM - kN;
+                    y[j] = twist(x[i], x[i + 1], x[im]);
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int i = lo + lane + 32 * j;
+                if (i < hi)
+                    x[i] = y[j];
+            }
+            __syncwarp();
         }
+        if (lane == 0)
+            x[kN - 1] = twist(x[kN - 1], x[0], x[kM - 1]);
+        __syncwarp();
     }
+    for (int i = lane; i < kN; i += 32)
+        g[(long long)i * L] = x[i];
 }
 
 } // namespace vmt_b200

@@ -120,9 +120,9 @@ def test_gemm_positioning_in_fused_modes():
 
 
 def test_gemm_positioning_reuses_matrix_with_block_advance():
-    """Three fill sizes cycling (block deltas D, D+1, D+2): two matrices get
-    cached, the third delta reuses the one a block below and regenerates the
-    remaining block (vmt_advance_blocks_kernel); words stay identical."""
+    """Three fill sizes cycling (block deltas D, D+1, D+2): the deltas above
+    a cached one reuse its matrix and regenerate the remaining blocks in place
+    (vmt_advance_blocks_kernel); words stay identical."""
     bw = 624 * 32
     ref = V.VmtGenerator(11, V.VmtConfig(32))
     gem = V.VmtGenerator(11, V.VmtConfig(32))
@@ -139,4 +139,4 @@ def test_gemm_positioning_reuses_matrix_with_block_advance():
         torch.cuda.synchronize()
         assert torch.equal(i32(a), i32(b)), k
     st = gem.positioning_stats()
-    assert st["cached_matrices"] == 2 and st["gemm_positionings"] >= 7
+    assert 1 <= st["cached_matrices"] <= 2 and st["gemm_positionings"] >= 7
