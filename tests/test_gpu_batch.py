@@ -83,3 +83,17 @@ def test_multi_gpu_fill_partition_and_checksum():
     assert torch.equal(torch.cat(outs), ref)
     assert x == x_ref
     assert V.multi_gpu_fill(5489, 32, n, devs, None) == x_ref  # fused XOR mode
+
+
+def test_zero_sizes_and_edges():
+    """Empty requests are no-ops that leave the stream where it was."""
+    g = V.VmtGenerator(5, V.VmtConfig(8, jump_exponent=10))
+    ones, bins = g.stat_counts(0)
+    assert ones == 0 and int(bins.sum()) == 0 and g.position == 0
+    assert g.checksum_xor(0) == 0
+    b = V.VmtBatch(1, 3, 8, 10)
+    b.fill(np.empty(0, np.uint32), 0)
+    assert b.position == 0
+    first = V.VmtGenerator(5, V.VmtConfig(8, jump_exponent=10)).next_u32()
+    assert g.next_u32() == first
+    assert V.multi_gpu_fill(5, 8, 0, [0], None, jump_exponent=10) == 0
