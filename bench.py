@@ -364,7 +364,10 @@ def main():
     T = args.words * world if args.scaling == "weak" else args.words
     start, count = partition(T, world, rank)
 
-    g = V.VmtGenerator(SEED, V.VmtConfig(LANES), device=local)
+    torch.cuda.synchronize(dev)
+    t_setup = time.perf_counter()
+    g = V.VmtGenerator(SEED, V.VmtConfig(LANES), device=local)  # seed + full-period de-phasing
+    setup_ms = (time.perf_counter() - t_setup) * 1e3
     g.set_tuning(max_chunks=args.chunks, variant=args.variant)
     out = torch.empty(count, dtype=torch.uint32, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -481,7 +484,7 @@ def main():
                    "parallelism": f"stream partition x{world} ({args.scaling})"},
         "gpu_launches": launches,
         "per_gpu_value": count / (ms * 1e-3),
-        "timing_breakdown_ms": {"gen_kernel": gen_ms, "positioning": jump_ms,
+        "timing_breakdown_ms": {"gen_kernel": gen_ms, "positioning": jump_ms, "setup_create": setup_ms,
                                 "positioning_gemms": g.positioning_stats()["gemm_positionings"],
                                 "note": "CUDA events on the fill's stream around the chunk positioning (steady "
                                         "state: one FP4 tensor-core GEMM (int8 fallback) mapping the previous "
