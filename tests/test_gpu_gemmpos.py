@@ -140,3 +140,24 @@ def test_gemm_positioning_reuses_matrix_with_block_advance():
         assert torch.equal(i32(a), i32(b)), k
     st = gem.positioning_stats()
     assert 1 <= st["cached_matrices"] <= 2 and st["gemm_positionings"] >= 7
+
+
+def test_gemm_positioned_stream_pinned_to_oracle(golden):
+    """The bench range [0, 2^34) produced in four consecutive 2^32-word calls
+    with GEMM positioning from the second call on: the XOR of all words (fused
+    checksums, and the stored words) equals the C oracle's pinned value."""
+    from test_gpu_parity import xor_reduce_inplace
+    c = golden["c4_full"]
+    g = V.VmtGenerator(c["seed"], V.VmtConfig(c["lanes"]))
+    g.set_positioning(2)
+    x = 0
+    for _ in range(4):
+        x ^= g.checksum_xor(1 << 32)
+    assert x == c["xor"] and g.positioning_stats()["gemm_positionings"] >= 3
+    g = V.VmtGenerator(c["seed"], V.VmtConfig(c["lanes"]))
+    g.set_positioning(2)
+    out = torch.empty(c["count"], dtype=torch.uint32, device="cuda")
+    for k in range(4):
+        g.fill_u32(out[k << 32:(k + 1) << 32])
+    assert g.positioning_stats()["gemm_positionings"] >= 3
+    assert xor_reduce_inplace(out) == c["xor"]
