@@ -219,6 +219,10 @@ int vmt_set_prefetch(vmt_handle h, int enable);
  * only, 2 = GEMM whenever the shape repeats. Results are identical. */
 int vmt_set_positioning(vmt_handle h, int mode);
 int vmt_positioning_stats(vmt_handle h, uint64_t* gemm_positionings, uint64_t* cached_matrices);
+/* De-phasing of many generators at once (vmt_batch_*, >= 4096 lane states)
+ * runs as log2(lanes) FP4 GEMMs with a process-wide cache of the jump
+ * matrices F^(s 2^q) per device (200 MB each, at most 8); this frees it. */
+int vmt_release_caches(int device);
 
 /* Profiling: when enabled, each fill records CUDA events on its stream around
  * the chunk-positioning jumps and the generation kernel; vmt_last_timings

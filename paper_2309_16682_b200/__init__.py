@@ -35,7 +35,7 @@ __all__ = [
     "write_jump_matrix_file", "read_jump_matrix_file", "compute_jump_matrix", "jump_matrix_file_name",
     "vec_mat_mul", "jump_state_matrix", "StatReport", "monobit", "chi2_bytes", "stat_counts",
     "regularized_gamma_q", "K_SIGNIFICANCE", "lane_cross_correlation", "monobit_from_counts",
-    "chi2_bytes_from_counts", "VmtBatch", "multi_gpu_fill", "store_bandwidth",
+    "chi2_bytes_from_counts", "VmtBatch", "multi_gpu_fill", "store_bandwidth", "release_caches",
 ]
 
 KSTATE_LEN = 624
@@ -368,6 +368,11 @@ class VmtBatch:
         out = np.empty((self.ngen, KSTATE_LEN * self.lanes), np.uint32)
         check(lib.vmt_batch_export_state(self._h, out.ctypes.data))
         return out
+
+
+def release_caches(device: int = 0) -> None:
+    """Frees the process-wide de-phasing matrix cache of a device."""
+    check(lib.vmt_release_caches(device))
 
 
 def store_bandwidth(bytes_: int = 1 << 34, pattern: int = 0, ctas_per_sm: int = 2, device: int = 0) -> float:

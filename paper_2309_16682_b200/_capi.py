@@ -30,7 +30,7 @@ EXPORTS = [
     "vmt_monobit_from_counts", "vmt_chi2_bytes_from_counts", "vmt_lane_cross_correlation",
     "vmt_batch_create", "vmt_batch_fill", "vmt_batch_skip", "vmt_batch_position", "vmt_batch_export_state",
     "vmt_batch_destroy", "vmt_multi_gpu_fill", "vmt_store_bandwidth",
-    "vmt_set_positioning", "vmt_positioning_stats",
+    "vmt_set_positioning", "vmt_positioning_stats", "vmt_release_caches",
 ]
 
 
@@ -123,6 +123,7 @@ def _load() -> ctypes.CDLL:
         "vmt_batch_export_state": (c.c_int, [H, c.c_void_p]),
         "vmt_batch_destroy": (c.c_int, [H]),
         "vmt_set_positioning": (c.c_int, [H, c.c_int]),
+        "vmt_release_caches": (c.c_int, [c.c_int]),
         "vmt_positioning_stats": (c.c_int, [H, u64p, u64p]),
         "vmt_store_bandwidth": (c.c_int, [c.c_int, c.c_uint64, c.c_int, c.c_int, c.POINTER(c.c_double)]),
         "vmt_multi_gpu_fill": (c.c_int, [c.c_uint32, c.c_uint, c.c_uint, c.c_uint64, c.c_int,

@@ -124,6 +124,25 @@ bool lt_fp4_gemm(GemmPos& gp, const void* mat, const void* bits, float* prod, st
     return ok;
 }
 
+// p(F) in word-bit coordinates as the GEMM's A operand: FP4 ([out][in], two
+// per byte) or int8.
+void build_gemm_matrix(const Poly& poly, bool fp4, DevBuf<std::int8_t>& m, cudaStream_t st) {
+    DevBuf<std::uint64_t> rows;
+    rows.reserve(kMatWords);
+    Counters cnt;
+    matrix_from_poly(poly, rows.p, st, cnt);
+    if (fp4) {
+        m.reserve(kGemmMatBytes / 2);
+        vmt_gemm_matrix_fp4_kernel<<<dim3((kWB / 2 + 255) / 256, kWB), 256, 0, st>>>(
+            rows.p, reinterpret_cast<std::uint8_t*>(m.p));
+    } else {
+        m.reserve(kGemmMatBytes);
+        vmt_gemm_matrix_kernel<<<dim3((kWB + 255) / 256, kWB), 256, 0, st>>>(rows.p, m.p);
+    }
+    VMT_CUDA(cudaGetLastError());
+    VMT_CUDA(cudaStreamSynchronize(st)); // rows is released on return
+}
+
 // The matrix for a delta, building it when there is room: at most two are
 // cached, and one is only replaced after 32 positionings without a use -- so
 // sizes that wander cannot turn every fill into a 10 ms matrix build.
@@ -151,21 +170,8 @@ const std::int8_t* gemm_matrix(vmt_generator* h, GemmPos& gp, std::uint64_t delt
     }
     Gf2Field& F = Gf2Field::instance();
     const unsigned __int128 d = (unsigned __int128)kN * delta;
-    DevBuf<std::uint64_t> rows;
-    rows.reserve(kMatWords);
-    Counters cnt;
-    matrix_from_poly(F.x_pow128((std::uint64_t)d, (std::uint64_t)(d >> 64)), rows.p, st, cnt);
     std::unique_ptr<DevBuf<std::int8_t>> m(new DevBuf<std::int8_t>());
-    if (gp.fp4 == 1) {
-        m->reserve(kGemmMatBytes / 2);
-        vmt_gemm_matrix_fp4_kernel<<<dim3((kWB / 2 + 255) / 256, kWB), 256, 0, st>>>(
-            rows.p, reinterpret_cast<std::uint8_t*>(m->p));
-    } else {
-        m->reserve(kGemmMatBytes);
-        vmt_gemm_matrix_kernel<<<dim3((kWB + 255) / 256, kWB), 256, 0, st>>>(rows.p, m->p);
-    }
-    VMT_CUDA(cudaGetLastError());
-    VMT_CUDA(cudaStreamSynchronize(st)); // rows is released on return
+    build_gemm_matrix(F.x_pow128((std::uint64_t)d, (std::uint64_t)(d >> 64)), gp.fp4 == 1, *m, st);
     h->cnt.other += 1;
     const std::int8_t* p = m->p;
     gp.mats[delta] = std::move(m);
@@ -231,12 +237,12 @@ bool gemm_position_exact(vmt_generator* h, GemmPos& gp, const std::uint32_t* src
         gp.prod.reserve(rows_pad * kWB);
         if (rows_pad > rows)
             VMT_CUDA(cudaMemsetAsync(gp.a.p + rows * kWB / 2, 0, (rows_pad - rows) * kWB / 2, st));
-        vmt_states_to_fp4_kernel<<<grid, 256, 0, st>>>(src, (int)h->L, nwords,
+        vmt_states_to_fp4_kernel<<<grid, 256, 0, st>>>(src, (int)h->L, 0, (int)h->L, nwords,
                                                         reinterpret_cast<std::uint8_t*>(gp.a.p));
         VMT_CUDA(cudaGetLastError());
         float* prod = reinterpret_cast<float*>(gp.prod.p);
         if (lt_fp4_gemm(gp, mat, gp.a.p, prod, rows_pad, st)) {
-            vmt_f32_to_states_kernel<<<grid, 256, 0, st>>>(prod, (int)h->L, nwords, dst);
+            vmt_f32_to_states_kernel<<<grid, 256, 0, st>>>(prod, (int)h->L, 0, (int)h->L, nwords, dst);
             VMT_CUDA(cudaGetLastError());
             h->cnt.other += 2; // expand + pack (the GEMM itself is cuBLASLt's kernel)
             h->cnt.gemm_positionings += 1;
@@ -272,6 +278,80 @@ bool gemm_position_exact(vmt_generator* h, GemmPos& gp, const std::uint32_t* src
     VMT_CUDA(cudaGetLastError());
     h->cnt.other += 2; // expand + pack (the GEMM itself is cuBLAS's kernel)
     h->cnt.gemm_positionings += 1;
+    return true;
+}
+
+// ---- de-phasing many generators at once (config 3) -------------------------
+// Lanes [s, s+n) of every generator = lanes [0, n) x F^(s 2^q): log2(L) FP4
+// GEMMs (s = 1, 2, 4, ...) with a process-wide cache of the matrices per
+// (device, q, s), instead of ngen*(L-1) polynomial jumps.
+struct DephaseGemm {
+    std::mutex mu;
+    GemmPos gp; // cuBLASLt handle, scales, workspace, operand buffers
+    std::map<std::pair<unsigned, unsigned>, std::unique_ptr<DevBuf<std::int8_t>>> mats;
+    bool fp4_ok = true;
+};
+
+std::mutex g_dephase_mu;
+std::map<int, std::unique_ptr<DephaseGemm>> g_dephase;
+
+DephaseGemm& dephase_gemm(int dev) {
+    std::lock_guard<std::mutex> lk(g_dephase_mu);
+    auto& slot = g_dephase[dev];
+    if (!slot)
+        slot.reset(new DephaseGemm());
+    return *slot;
+}
+
+// states: [ngen][624][L], lane 0 seeded; fills lanes 1..L-1. false: not done
+// (no FP4 GEMM here; the caller uses the polynomial jumps).
+bool dephase_by_gemm(int device, cudaStream_t st, unsigned ngen, unsigned L, unsigned q, std::uint32_t* states,
+                     Counters& cnt) {
+    static const bool off = std::getenv("VMT_GEMM_INT8") != nullptr; // FP4 only here
+    if (off || L < 2)
+        return false;
+    DephaseGemm& D = dephase_gemm(device);
+    std::lock_guard<std::mutex> lk(D.mu);
+    if (!D.fp4_ok)
+        return false;
+    Gf2Field& F = Gf2Field::instance();
+    for (unsigned s = 1; s < L; s *= 2) {
+        const unsigned n = std::min(s, L - s);
+        auto key = std::make_pair(q, s);
+        auto it = D.mats.find(key);
+        if (it == D.mats.end()) {
+            if (D.mats.size() >= 8) {
+                VMT_CUDA(cudaStreamSynchronize(st));
+                D.mats.clear();
+            }
+            std::unique_ptr<DevBuf<std::int8_t>> m(new DevBuf<std::int8_t>());
+            build_gemm_matrix(F.powmod(F.x_pow2(q), s), true, *m, st);
+            cnt.other += 1;
+            it = D.mats.emplace(key, std::move(m)).first;
+        }
+        const std::uint64_t rows = (std::uint64_t)ngen * n, rows_pad = (rows + 127) / 128 * 128;
+        const long long nwords = (long long)rows * kN;
+        const unsigned grid = (unsigned)((nwords + 255) / 256);
+        D.gp.a.reserve(rows_pad * kWB / 2);
+        D.gp.prod.reserve(rows_pad * kWB);
+        if (rows_pad > rows)
+            VMT_CUDA(cudaMemsetAsync(D.gp.a.p + rows * kWB / 2, 0, (rows_pad - rows) * kWB / 2, st));
+        vmt_states_to_fp4_kernel<<<grid, 256, 0, st>>>(states, (int)L, 0, (int)n, nwords,
+                                                        reinterpret_cast<std::uint8_t*>(D.gp.a.p));
+        VMT_CUDA(cudaGetLastError());
+        float* prod = reinterpret_cast<float*>(D.gp.prod.p);
+        if (!lt_fp4_gemm(D.gp, it->second->p, D.gp.a.p, prod, rows_pad, st)) {
+            D.fp4_ok = false;
+            VMT_CUDA(cudaStreamSynchronize(st));
+            if (s == 1)
+                return false; // nothing written yet: the caller jumps instead
+            throw VmtError(VMT_ECUDA, "FP4 GEMM failed during de-phasing");
+        }
+        vmt_f32_to_states_kernel<<<grid, 256, 0, st>>>(prod, (int)L, (int)s, (int)n, nwords, states);
+        VMT_CUDA(cudaGetLastError());
+        cnt.other += 2;
+    }
+    VMT_CUDA(cudaStreamSynchronize(st));
     return true;
 }
 

@@ -903,6 +903,14 @@ void build_dephased(int device, cudaStream_t st, std::uint32_t seed0, unsigned n
     vmt_seed_kernel<<<(ngen + 127) / 128, 128, 0, st>>>(dseeds.p, (int)ngen, dst, (long long)kN * L, (int)L);
     VMT_CUDA(cudaGetLastError());
     cnt.other += 1;
+    // many generators: log2(L) tensor-core GEMMs with cached matrices
+    static const std::uint64_t gemm_min = std::getenv("VMT_DEPHASE_GEMM_MIN")
+                                              ? std::strtoull(std::getenv("VMT_DEPHASE_GEMM_MIN"), nullptr, 10)
+                                              : 4096;
+    if (L > 1 && (std::uint64_t)ngen * (L - 1) >= gemm_min && dephase_by_gemm(device, st, ngen, L, q, dst, cnt)) {
+        VMT_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
     if (L > 1) {
         const std::vector<Poly> polys = dephase_polys(q, L);
         polybuf.reserve(polys.size() * kPolyWords);
@@ -1340,6 +1348,20 @@ int vmt_set_prefetch(vmt_handle h, int enable) {
         require(h != nullptr, VMT_EINVAL, "null handle");
         h->prefetch = enable != 0;
         h->pref_valid = false;
+    });
+}
+
+int vmt_release_caches(int device) {
+    return guarded([&] {
+        check_device(device);
+        DeviceGuard g(device);
+        VMT_CUDA(cudaDeviceSynchronize());
+        std::lock_guard<std::mutex> lk(g_dephase_mu);
+        auto it = g_dephase.find(device);
+        if (it != g_dephase.end()) {
+            std::lock_guard<std::mutex> lk2(it->second->mu);
+            it->second->mats.clear();
+        }
     });
 }
 

@@ -238,16 +238,19 @@ __global__ void vmt_gemm_matrix_fp4_kernel(const std::uint64_t* __restrict__ row
     mwt[(long long)jc * (kWB / 2) + ip2] = v;
 }
 
-__global__ void vmt_states_to_fp4_kernel(const std::uint32_t* __restrict__ st, int L, long long nwords,
-                                         std::uint8_t* __restrict__ a) {
+// a[r][.] for r = c*nl + j: lane lane0+j of state c of an interleaved
+// [C][624][L] array (nl = L, lane0 = 0: every lane state).
+__global__ void vmt_states_to_fp4_kernel(const std::uint32_t* __restrict__ st, int L, int lane0, int nl,
+                                         long long nwords, std::uint8_t* __restrict__ a) {
     const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= nwords)
         return;
-    const int t = (int)(idx % L);
-    const long long ck = idx / L;
+    const int j = (int)(idx % nl);
+    const long long ck = idx / nl;
     const int k = (int)(ck % kN);
-    const long long r = (ck / kN) * L + t;
-    std::uint32_t w = st[idx];
+    const long long c = ck / kN;
+    const long long r = c * nl + j;
+    std::uint32_t w = st[(c * kN + k) * L + lane0 + j];
     if (k == 0)
         w &= kUpperMask;
     // byte n holds bits 2n (low nibble) and 2n+1 (high nibble) as code 0x2
@@ -265,15 +268,17 @@ __global__ void vmt_states_to_fp4_kernel(const std::uint32_t* __restrict__ st, i
     *reinterpret_cast<uint4*>(a + r * (kWB / 2) + 16 * k) = make_uint4(q[0], q[1], q[2], q[3]);
 }
 
-__global__ void vmt_f32_to_states_kernel(const float* __restrict__ prod, int L, long long nwords,
+// inverse: row r = c*nl + j of the fp32 product -> lane lane0+j of state c
+__global__ void vmt_f32_to_states_kernel(const float* __restrict__ prod, int L, int lane0, int nl, long long nwords,
                                          std::uint32_t* __restrict__ st) {
     const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= nwords)
         return;
-    const int t = (int)(idx % L);
-    const long long ck = idx / L;
+    const int j = (int)(idx % nl);
+    const long long ck = idx / nl;
     const int k = (int)(ck % kN);
-    const long long r = (ck / kN) * L + t;
+    const long long c = ck / kN;
+    const long long r = c * nl + j;
     const float4* src = reinterpret_cast<const float4*>(prod + r * kWB + 32 * k);
     std::uint32_t w = 0;
 #pragma unroll
@@ -282,7 +287,7 @@ __global__ void vmt_f32_to_states_kernel(const float* __restrict__ prod, int L, 
         w |= ((std::uint32_t)(int)v.x & 1u) << (4 * n) | ((std::uint32_t)(int)v.y & 1u) << (4 * n + 1) |
              ((std::uint32_t)(int)v.z & 1u) << (4 * n + 2) | ((std::uint32_t)(int)v.w & 1u) << (4 * n + 3);
     }
-    st[idx] = k == 0 ? (w & kUpperMask) : w;
+    st[(c * kN + k) * L + lane0 + j] = k == 0 ? (w & kUpperMask) : w;
 }
 
 } // namespace vmt_b200
