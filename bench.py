@@ -278,7 +278,7 @@ def extras(dev) -> dict:
     b3 = torch.empty(1024 * n, dtype=torch.uint32, device=dev)
     s = timed(lambda: V.batch_fill_u32(b3, 1, 1024, 16, n), reps=2)
     out["c3_1024xL16_2p20_u32"] = {"value": 1024 * n / s, "unit": "uint32/s", "ms": s * 1e3,
-                                   "note": "includes seeding + 15360 full-period de-phasing jumps"}
+                                   "note": "includes seeding + de-phasing of 15360 lane states (four FP4 GEMMs, matrices cached)"}
     del b3
     # c5: 4096 states (seeds 1..4096) jumped by 64-bit distances, then 624 outputs each
     seeds = np.arange(1, 4097, dtype=np.uint32)
