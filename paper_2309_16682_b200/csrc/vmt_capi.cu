@@ -679,9 +679,18 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
             // build the 400 MB matrix only for a delta that repeats
             if (usable_base(gp, delta) || seen >= 2 || h->positioning == 2) {
                 h->chunks_alt.reserve((size_t)C * kN * h->L);
-                if (gemm_position(h, gp, h->chunks.p, h->chunks_alt.p, C * h->L, delta, st)) {
-                    h->chunks.swap(h->chunks_alt);
-                    positioned = true;
+                try {
+                    if (gemm_position(h, gp, h->chunks.p, h->chunks_alt.p, C * h->L, delta, st)) {
+                        h->chunks.swap(h->chunks_alt);
+                        positioned = true;
+                    }
+                } catch (const VmtError&) {
+                    // e.g. no memory for the matrix / operands: use the jumps
+                    // from now on (the chunk states are rebuilt below)
+                    cudaGetLastError();
+                    VMT_CUDA(cudaStreamSynchronize(st));
+                    gp.mats.clear();
+                    h->positioning = 1;
                 }
             }
         }
@@ -907,9 +916,18 @@ void build_dephased(int device, cudaStream_t st, std::uint32_t seed0, unsigned n
     static const std::uint64_t gemm_min = std::getenv("VMT_DEPHASE_GEMM_MIN")
                                               ? std::strtoull(std::getenv("VMT_DEPHASE_GEMM_MIN"), nullptr, 10)
                                               : 4096;
-    if (L > 1 && (std::uint64_t)ngen * (L - 1) >= gemm_min && dephase_by_gemm(device, st, ngen, L, q, dst, cnt)) {
-        VMT_CUDA(cudaStreamSynchronize(st));
-        return;
+    if (L > 1 && (std::uint64_t)ngen * (L - 1) >= gemm_min) {
+        bool done = false;
+        try {
+            done = dephase_by_gemm(device, st, ngen, L, q, dst, cnt);
+        } catch (const VmtError&) { // e.g. no memory for the matrices: jump instead
+            cudaGetLastError();
+            VMT_CUDA(cudaStreamSynchronize(st));
+        }
+        if (done) {
+            VMT_CUDA(cudaStreamSynchronize(st));
+            return;
+        }
     }
     if (L > 1) {
         const std::vector<Poly> polys = dephase_polys(q, L);
