@@ -107,8 +107,16 @@ struct GenShape {
     }
     // registers are capped so that they never limit occupancy below that
     template <int MODE>
+    // (the 32-lane store shape runs one CTA per SM anyway -- one chunk per SM
+    // is what the planner picks -- and is 3% faster without the 128-register
+    // cap; the fused modes are not)
     __host__ __device__ static constexpr int minb() {
-        return (smem_ctas<MODE>() * NT > 2048) ? (2048 / NT > 0 ? 2048 / NT : 1) : smem_ctas<MODE>();
+#ifdef VMT_GEN_MINB
+        return VMT_GEN_MINB;
+#endif
+        return (L == 32 && NT == 256 && MODE != MODE_XOR && MODE != MODE_STATS && MODE != MODE_BENCH_TEMPER_XOR)
+                   ? 1
+                   : (smem_ctas<MODE>() * NT > 2048) ? (2048 / NT > 0 ? 2048 / NT : 1) : smem_ctas<MODE>();
     }
     static_assert(W % R == 0 && kN % W == 0 && RING % R == 0 && W <= 227, "bad window / run length");
     static_assert(!TMA || RING_BYTES % 16 == 0, "staging alignment");
