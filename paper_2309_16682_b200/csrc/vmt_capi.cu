@@ -391,6 +391,7 @@ struct vmt_generator {
     bool pref_valid = false;
     std::uint64_t pref_b0 = 0, pref_B = 0, pref_C = 0;
     std::uint64_t last_end = ~0ull;  // end position of the previous GPU fill
+    std::uint64_t last_fill_n = 0;   // size of the previous GPU fill
     cudaStream_t side = nullptr;     // prefetch stream
     cudaEvent_t ev_chunks = nullptr, ev_pref = nullptr;
     DevBuf<std::uint32_t> partials;  // per-CTA xor partials
@@ -584,7 +585,13 @@ cudaEvent_t* prof_next(vmt_generator* h) {
 // words/s, an SM's store path saturates at ~1.6e12 / 148 words/s. Past one
 // chunk per SM only whole waves (multiples of sms) are candidates: a partial
 // wave leaves the SMs with one chunk more as the tail.
-std::uint64_t plan_chunks(unsigned L, std::uint64_t n, std::uint64_t c_max, int sms) {
+//
+// Fused XOR fills (no stores) run at ~5.5e8 words/s per lane and saturate at
+// ~3.4e12 words/s per GPU; and when the previous fill had the same size the
+// positioning is one GEMM (capi_gemmpos.inl, ~0.12 ms + 0.14 us per lane
+// state) rather than jumps.
+std::uint64_t plan_chunks(unsigned L, std::uint64_t n, std::uint64_t c_max, int sms, int mode = MODE_U32,
+                          bool gemm = false) {
     const double per_jump = 0.43e-6 * 148.0 / (double)sms;
     auto t_jump = [&](double jobs) -> double {
         if (jobs <= 0)
@@ -592,10 +599,17 @@ std::uint64_t plan_chunks(unsigned L, std::uint64_t n, std::uint64_t c_max, int 
         const double floor_s = jobs <= sms * 4.0 ? 0.16e-3 : (jobs <= sms * 16.0 ? 0.37e-3 : 0.0);
         return std::max(floor_s, jobs * per_jump);
     };
-    const double r_lane = 3.2e8, peak_sm = 1.6e12 / 148.0;
+    const bool fused = mode == MODE_XOR;
+    const double r_lane = fused ? 5.5e8 : 3.2e8, peak_sm = (fused ? 3.4e12 : 1.6e12) / 148.0;
+    auto t_pos = [&](std::uint64_t C) -> double {
+        const double rows = double(C) * L;
+        if (gemm && rows >= (double)gemm_min_rows())
+            return std::min(t_jump(double(C - 1) * L), 0.12e-3 + rows * 1.4e-7 * 148.0 / (double)sms);
+        return t_jump(double(C - 1) * L);
+    };
     auto t = [&](std::uint64_t C) {
         const double k = (double)((C + sms - 1) / sms);
-        return t_jump(double(C - 1) * L) + (double(n) / double(C)) / std::min(L * r_lane, peak_sm / k);
+        return t_pos(C) + (double(n) / double(C)) / std::min(L * r_lane, peak_sm / k);
     };
     std::uint64_t best = 1;
     double tb = t(1);
@@ -646,7 +660,11 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     const int sms = device_info(h->device).sms;
     const std::uint64_t max_grid = (std::uint64_t)sms * occ;
     const std::uint64_t c_max = std::min<std::uint64_t>(std::max<std::uint64_t>(1, max_grid / groups), nb);
-    std::uint64_t C = h->max_chunks ? std::min<std::uint64_t>(c_max, h->max_chunks) : plan_chunks(h->L, n, c_max, sms);
+    // a fill of the same size as the previous one is likely to repeat: plan
+    // with the GEMM positioning cost
+    const bool gemm_plan = h->positioning != 1 && h->last_fill_n == n;
+    std::uint64_t C = h->max_chunks ? std::min<std::uint64_t>(c_max, h->max_chunks)
+                                    : plan_chunks(h->L, n, c_max, sms, mode, gemm_plan);
     static const bool debug = std::getenv("VMT_DEBUG") != nullptr;
     if (debug)
         std::fprintf(stderr, "[vmt] L=%u R=%d NT=%d smem=%d occ=%d chunks=%llu blocks=%llu mode=%d vec=%d\n", h->L,
@@ -730,7 +748,7 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
         const std::uint64_t nbn = (P0n + n + h->bw - 1) / h->bw - next_b0;
         const std::uint64_t c_max_n = std::min<std::uint64_t>(std::max<std::uint64_t>(1, max_grid / groups), nbn);
         std::uint64_t Cn = h->max_chunks ? std::min<std::uint64_t>(c_max_n, h->max_chunks)
-                                         : plan_chunks(h->L, n, c_max_n, sms);
+                                         : plan_chunks(h->L, n, c_max_n, sms, mode, gemm_plan);
         const std::uint64_t Bn = (nbn + Cn - 1) / Cn;
         Cn = (nbn + Bn - 1) / Bn;
         prefetch_now = Cn == C && Bn == B && next_b0 >= b0;
@@ -788,6 +806,7 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
         h->pref_C = C;
     }
     h->last_end = P1;
+    h->last_fill_n = n;
     if (pe)
         VMT_CUDA(cudaEventRecord(pe[2], st));
     if (mode == MODE_XOR) {

@@ -153,7 +153,7 @@ def test_gemm_positioned_stream_pinned_to_oracle(golden):
     x = 0
     for _ in range(4):
         x ^= g.checksum_xor(1 << 32)
-    assert x == c["xor"] and g.positioning_stats()["gemm_positionings"] >= 3
+    assert x == c["xor"] and g.positioning_stats()["gemm_positionings"] >= 2
     g = V.VmtGenerator(c["seed"], V.VmtConfig(c["lanes"]))
     g.set_positioning(2)
     out = torch.empty(c["count"], dtype=torch.uint32, device="cuda")
