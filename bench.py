@@ -422,8 +422,9 @@ def main():
     # -- end to end, fused consumer: the step's result is the 4-byte XOR
     # checksum read back to the host (config 4's no-store mode)
     g.seek(start)
-    g.checksum_xor(count)
-    g.skip(T - count)
+    for _ in range(args.warmup):  # same warm-up as the timed store steps
+        g.checksum_xor(count)
+        g.skip(T - count)
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
