@@ -204,12 +204,23 @@ int vmt_create_from_file(uint32_t seed, unsigned lanes, const char* path, int de
 /* Kernel tuning for the generation path: chunks per fill (0 = auto), and
  * the CTA shape variant (0 = auto). Returns VMT_EINVAL for unknown variants. */
 int vmt_set_tuning(vmt_handle h, unsigned max_chunks, int variant);
-/* Steady-state positioning prefetch (default off: with the generation kernel
- * ALU-saturated the overlapped jumps slow it by as much as they save, see
- * DESIGN.md section 5): while a fill of >= 2^24
- * words generates, the chunk start states of the predicted next fill (same
- * size, same gap) are computed on a side stream; a matching next fill skips
- * its positioning jumps. Results are identical either way. */
+/* Steady-state positioning prefetch: while a fill of >= 2^24 words
+ * generates, the chunk start states of the predicted next fill (same size,
+ * same gap) are computed on a side stream; a matching next fill skips its
+ * positioning. Results are identical in every mode.
+ *   VMT_PREFETCH_OFF     none
+ *   VMT_PREFETCH_JUMPS   polynomial jumps on the side stream (with the
+ *                        generation kernel ALU-saturated they slow it by as
+ *                        much as they save)
+ *   VMT_PREFETCH_TENSOR  default: one tcgen05 GEMM with the cached positioning
+ *                        matrix, co-resident with the generation kernel on the
+ *                        idle tensor cores (once the fill shape repeats and the
+ *                        generation kernel leaves room on every SM; otherwise
+ *                        the fill is positioned as without prefetch)
+ * Returns VMT_EINVAL for other values. */
+#define VMT_PREFETCH_OFF 0
+#define VMT_PREFETCH_JUMPS 1
+#define VMT_PREFETCH_TENSOR 2
 int vmt_set_prefetch(vmt_handle h, int enable);
 
 /* Chunk positioning of consecutive fills: mode 0 =
@@ -219,6 +230,9 @@ int vmt_set_prefetch(vmt_handle h, int enable);
  * only, 2 = GEMM whenever the shape repeats. Results are identical. */
 int vmt_set_positioning(vmt_handle h, int mode);
 int vmt_positioning_stats(vmt_handle h, uint64_t* gemm_positionings, uint64_t* cached_matrices);
+/* Prefetch counters: tcgen05 prefetch launches (VMT_PREFETCH_TENSOR) and
+ * fills that used prefetched chunk states (any mode). */
+int vmt_prefetch_stats(vmt_handle h, uint64_t* tensor_prefetches, uint64_t* used);
 /* De-phasing of many generators at once (vmt_batch_*, >= 4096 lane states)
  * runs as log2(lanes) FP4 GEMMs with a process-wide cache of the jump
  * matrices F^(s 2^q) per device (200 MB each, at most 8); this frees it. */

@@ -269,8 +269,15 @@ class VmtGenerator:
     def set_tuning(self, max_chunks: int = 0, variant: int = 0) -> None:
         check(lib.vmt_set_tuning(self._h, max_chunks, variant))
 
-    def set_prefetch(self, enable: bool = True) -> None:
-        check(lib.vmt_set_prefetch(self._h, int(enable)))
+    def set_prefetch(self, mode: int = 1) -> None:
+        """0 off, 1 (or True) polynomial jumps on a side stream, 2 tcgen05 GEMM
+        beside the generation kernel (the default)."""
+        check(lib.vmt_set_prefetch(self._h, int(mode)))
+
+    def prefetch_stats(self) -> dict:
+        t, u = ctypes.c_uint64(), ctypes.c_uint64()
+        check(lib.vmt_prefetch_stats(self._h, ctypes.byref(t), ctypes.byref(u)))
+        return {"tensor_prefetches": t.value, "used": u.value}
 
     def set_positioning(self, mode: int = 0) -> None:
         """0 auto (GEMM for repeating fill shapes), 1 polynomial jumps, 2 GEMM."""

@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(PKG, "libvmt19937_b200.so")
 
 VMT_OK, VMT_EINVAL, VMT_ESTATE, VMT_EIO, VMT_ECUDA, VMT_ENOMEM = 0, -1, -2, -3, -4, -5
 VMT_FULL_PERIOD = 0xFFFFFFFF
+VMT_PREFETCH_OFF, VMT_PREFETCH_JUMPS, VMT_PREFETCH_TENSOR = 0, 1, 2
 VMT_F32_24, VMT_F64_32, VMT_F64_REAL3, VMT_F64_RES53 = 0, 1, 2, 3
 
 # every symbol include/vmt19937_b200.h declares
@@ -22,7 +23,7 @@ EXPORTS = [
     "vmt_state_words", "vmt_jump_exponent", "vmt_position", "vmt_next_u32", "vmt_next_block16",
     "vmt_next_block_state", "vmt_fill_u32", "vmt_fill_f32", "vmt_fill_f64", "vmt_checksum_xor",
     "vmt_skip", "vmt_seek", "vmt_synchronize", "vmt_export_state", "vmt_batch_fill_u32", "vmt_jump_states", "vmt_seed_states",
-    "vmt_jump_poly", "vmt_jump_poly_pow2", "vmt_charpoly", "vmt_set_tuning", "vmt_set_prefetch", "vmt_set_profiling", "vmt_last_timings", "vmt_profile_totals", "vmt_stats",
+    "vmt_jump_poly", "vmt_jump_poly_pow2", "vmt_charpoly", "vmt_set_tuning", "vmt_set_prefetch", "vmt_prefetch_stats", "vmt_set_profiling", "vmt_last_timings", "vmt_profile_totals", "vmt_stats",
     "vmt_status_string", "vmt_last_error", "vmt_version",
     "vmt_jump_matrix", "vmt_jump_matrix_pow2", "vmt_write_jump_matrix_file", "vmt_read_jump_matrix_file",
     "vmt_compute_jump_matrix_file", "vmt_vec_mat_mul", "vmt_jump_states_matrix", "vmt_create_from_matrix",
@@ -92,6 +93,7 @@ def _load() -> ctypes.CDLL:
         "vmt_charpoly": (c.c_int, [c.c_void_p]),
         "vmt_set_tuning": (c.c_int, [H, c.c_uint, c.c_int]),
         "vmt_set_prefetch": (c.c_int, [H, c.c_int]),
+        "vmt_prefetch_stats": (c.c_int, [H, u64p, u64p]),
         "vmt_stats": (c.c_int, [H, u64p, u64p, u64p, u64p]),
         "vmt_set_profiling": (c.c_int, [H, c.c_int]),
         "vmt_last_timings": (c.c_int, [H, c.POINTER(c.c_float), c.POINTER(c.c_float)]),

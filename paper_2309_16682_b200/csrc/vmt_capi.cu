@@ -130,12 +130,51 @@ int prepare_gen(int dev, GenFn fn, int nt, int smem) {
     const void* key = reinterpret_cast<const void*>(fn);
     if (!d.smem_set.count(key)) {
         VMT_CUDA(cudaFuncSetAttribute(key, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        if (std::getenv("VMT_FORCE_CARVEOUT")) // experiment knob
+            VMT_CUDA(cudaFuncSetAttribute(key, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         int occ = 0;
         VMT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, key, nt, smem));
         d.occ[key] = std::max(occ, 1);
         d.smem_set.insert(key);
     }
     return d.occ[key];
+}
+
+// Whether one vmt_posmma_kernel CTA fits on an SM beside one CTA of the
+// generation kernel `fn` (shared memory incl. the 1 KB per-CTA reservation,
+// registers, threads).
+bool posmma_fits(int dev, GenFn fn, int nt, int smem) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, bool> memo;
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair(dev, reinterpret_cast<const void*>(fn));
+    auto it = memo.find(key);
+    if (it != memo.end())
+        return it->second;
+    int sm_smem = 0, sm_regs = 0, sm_threads = 0;
+    VMT_CUDA(cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+    VMT_CUDA(cudaDeviceGetAttribute(&sm_regs, cudaDevAttrMaxRegistersPerMultiprocessor, dev));
+    VMT_CUDA(cudaDeviceGetAttribute(&sm_threads, cudaDevAttrMaxThreadsPerMultiProcessor, dev));
+    cudaFuncAttributes ga{}, pa{};
+    VMT_CUDA(cudaFuncGetAttributes(&ga, reinterpret_cast<const void*>(fn)));
+    VMT_CUDA(cudaFuncGetAttributes(&pa, reinterpret_cast<const void*>(vmt_posmma_kernel)));
+    auto regs = [](int per_thread, int threads) { // allocation unit: 256 registers per warp
+        return ((per_thread * 32 + 255) / 256 * 256) * ((threads + 31) / 32);
+    };
+    const bool ok = smem + 1024 + kPmSmem + 1024 <= sm_smem &&
+                    regs(ga.numRegs, nt) + regs(pa.numRegs, kPmThreads) <= sm_regs &&
+                    nt + kPmThreads <= sm_threads && !std::getenv("VMT_NO_TC_PREFETCH");
+    if (ok) {
+        // both kernels ask for the full shared-memory carveout: an SM whose
+        // generation CTA ran with the smallest carveout that fits it (132 KB)
+        // would have no room left for the GEMM CTA
+        VMT_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                      cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        VMT_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(vmt_posmma_kernel),
+                                      cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    }
+    memo[key] = ok;
+    return ok;
 }
 
 // ------------------------------------------------------- device buffers --
@@ -275,7 +314,7 @@ bool is_device_ptr(const void* p) {
 }
 
 struct Counters {
-    std::uint64_t gen = 0, jump = 0, other = 0, lane_jumps = 0, gemm_positionings = 0;
+    std::uint64_t gen = 0, jump = 0, other = 0, lane_jumps = 0, gemm_positionings = 0, tc_prefetches = 0, pref_used = 0;
 };
 
 // One CTA per job; with few jobs several warps split each job's coefficient
@@ -387,8 +426,9 @@ struct vmt_generator {
 
     DevBuf<std::uint32_t> chunks;    // [C][624][L]
     DevBuf<std::uint32_t> chunks_alt; // prefetched chunk states of the predicted next fill
-    bool prefetch = false;           // position the predicted next fill while this one generates
+    int prefetch = VMT_PREFETCH_OFF; // position the predicted next fill while this one generates
     bool pref_valid = false;
+    bool pref_inflight = false;      // ev_pref recorded and not yet waited for by a fill
     std::uint64_t pref_b0 = 0, pref_B = 0, pref_C = 0;
     std::uint64_t last_end = ~0ull;  // end position of the previous GPU fill
     std::uint64_t last_fill_n = 0;   // size of the previous GPU fill
@@ -681,17 +721,24 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     // by polynomial jumps from cur
     const bool use_pref = h->pref_valid && h->pref_b0 == b0 && h->pref_B == B && h->pref_C == C;
     h->pref_valid = false;
+    if (h->pref_inflight) {
+        // the side stream still reads h->chunks / writes h->chunks_alt
+        VMT_CUDA(cudaStreamWaitEvent(st, h->ev_pref, 0));
+        h->pref_inflight = false;
+    }
     bool positioned = false;
     if (use_pref) {
         // chunk 0 is the prefetched state at b0, so cur needs no re-positioning
         // (the generation kernel saves the next one)
-        VMT_CUDA(cudaStreamWaitEvent(st, h->ev_pref, 0));
         h->chunks.swap(h->chunks_alt);
         positioned = true;
+        h->cnt.pref_used += 1;
     }
     if (!positioned && h->positioning != 1 && C * h->L >= gemm_min_rows()) {
-        if (!h->gemm)
+        if (!h->gemm) {
             h->gemm = new GemmPos();
+            h->gemm->want_i8 = h->prefetch == VMT_PREFETCH_TENSOR;
+        }
         GemmPos& gp = *h->gemm;
         if (gp.last_valid && gp.last_B == B && gp.last_C == C && b0 > gp.last_b0) {
             const std::uint64_t delta = b0 - gp.last_b0;
@@ -745,7 +792,13 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     // the next fill is chunk c of this one advanced by the same block delta
     bool prefetch_now = false;
     std::uint64_t next_b0 = 0;
-    if (h->prefetch && C > 1 && n >= kPrefetchMinWords) {
+    const std::uint64_t grid = C * groups;
+    // the tensor-core form runs beside the generation kernel: only when that
+    // kernel leaves room for one vmt_posmma_kernel CTA on every SM it uses
+    const bool tc_pref = h->prefetch == VMT_PREFETCH_TENSOR && h->positioning != 1 && h->gemm &&
+                         C * h->L >= gemm_min_rows() && grid <= (std::uint64_t)sms && occ == 1 &&
+                         posmma_fits(h->device, fn, v.NT, smem);
+    if ((h->prefetch == VMT_PREFETCH_JUMPS || tc_pref) && C > 1 && n >= kPrefetchMinWords) {
         const std::uint64_t gap = (h->last_end != ~0ull && P0 >= h->last_end) ? P0 - h->last_end : 0;
         const std::uint64_t P0n = P1 + gap;
         next_b0 = P0n / h->bw;
@@ -765,7 +818,6 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
         }
         VMT_CUDA(cudaEventRecord(h->ev_chunks, st));
     }
-    const std::uint64_t grid = C * groups;
     if (pe)
         VMT_CUDA(cudaEventRecord(pe[1], st));
     if (mode == MODE_XOR)
@@ -789,6 +841,23 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     fn<<<(unsigned)grid, v.NT, smem, st>>>(p);
     VMT_CUDA(cudaGetLastError());
     h->cnt.gen += 1;
+    if (prefetch_now && tc_pref) {
+        // one tcgen05 GEMM with the cached int8 matrix of the next block delta,
+        // launched after the generation kernel so its CTAs take the resources
+        // the generation CTAs leave free on every SM
+        h->chunks_alt.reserve((size_t)C * kN * h->L);
+        VMT_CUDA(cudaStreamWaitEvent(h->side, h->ev_chunks, 0));
+        if (posmma_launch(*h->gemm, next_b0 - b0, h->chunks.p, h->chunks_alt.p, h->L, C * h->L, sms, h->side)) {
+            VMT_CUDA(cudaEventRecord(h->ev_pref, h->side));
+            h->pref_valid = true;
+            h->pref_inflight = true;
+            h->pref_b0 = next_b0;
+            h->pref_B = B;
+            h->pref_C = C;
+            h->cnt.tc_prefetches += 1;
+        }
+        prefetch_now = false;
+    }
     if (prefetch_now) {
         // launched after the generation kernel so its CTAs take the resources
         // the generation wave leaves free on every SM
@@ -805,6 +874,7 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
         launch_jumps_affine(h->side, h->chunks.p, (int)h->L, h->chunks_alt.p, (int)h->L, dp, a, h->cnt);
         VMT_CUDA(cudaEventRecord(h->ev_pref, h->side));
         h->pref_valid = true;
+        h->pref_inflight = true;
         h->pref_b0 = next_b0;
         h->pref_B = B;
         h->pref_C = C;
@@ -1046,13 +1116,13 @@ int vmt_destroy(vmt_handle h) {
             for (auto& t : h->evpool)
                 for (auto& e : t)
                     cudaEventDestroy(e);
-            delete h->gemm;
             if (h->side) {
                 cudaStreamSynchronize(h->side);
                 cudaStreamDestroy(h->side);
                 cudaEventDestroy(h->ev_chunks);
                 cudaEventDestroy(h->ev_pref);
             }
+            delete h->gemm;
             if (h->copy_stream) {
                 cudaStreamSynchronize(h->copy_stream);
                 cudaStreamDestroy(h->copy_stream);
@@ -1387,8 +1457,11 @@ int vmt_set_tuning(vmt_handle h, unsigned max_chunks, int variant) {
 int vmt_set_prefetch(vmt_handle h, int enable) {
     return guarded([&] {
         require(h != nullptr, VMT_EINVAL, "null handle");
-        h->prefetch = enable != 0;
+        require(enable >= VMT_PREFETCH_OFF && enable <= VMT_PREFETCH_TENSOR, VMT_EINVAL, "unknown prefetch mode");
+        h->prefetch = enable;
         h->pref_valid = false;
+        if (h->gemm)
+            h->gemm->want_i8 = enable == VMT_PREFETCH_TENSOR;
     });
 }
 
@@ -1421,6 +1494,16 @@ int vmt_positioning_stats(vmt_handle h, uint64_t* gemm_positionings, uint64_t* c
             *gemm_positionings = h->cnt.gemm_positionings;
         if (cached_matrices)
             *cached_matrices = h->gemm ? h->gemm->mats.size() : 0;
+    });
+}
+
+int vmt_prefetch_stats(vmt_handle h, uint64_t* tensor_prefetches, uint64_t* used) {
+    return guarded([&] {
+        require(h != nullptr, VMT_EINVAL, "null handle");
+        if (tensor_prefetches)
+            *tensor_prefetches = h->cnt.tc_prefetches;
+        if (used)
+            *used = h->cnt.pref_used;
     });
 }
 

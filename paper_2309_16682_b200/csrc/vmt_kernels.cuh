@@ -4,6 +4,7 @@
 //   vmt_jump.cuh    vmt_jump_kernel (polynomial jump-ahead), seeding, reduction
 //   vmt_matrix.cuh  GF(2) jump matrices: basis states, effective layout, vec_mat_mul
 //   vmt_diag.cuh    pure-store bandwidth probes (measurement only)
+//   vmt_posmma.cuh  tcgen05 positioning GEMM, co-resident with the generation kernel
 #pragma once
 
 #include "vmt_common.cuh"
@@ -11,3 +12,4 @@
 #include "vmt_jump.cuh"
 #include "vmt_matrix.cuh"
 #include "vmt_diag.cuh"
+#include "vmt_posmma.cuh"

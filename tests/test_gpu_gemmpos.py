@@ -161,3 +161,37 @@ def test_gemm_positioned_stream_pinned_to_oracle(golden):
         g.fill_u32(out[k << 32:(k + 1) << 32])
     assert g.positioning_stats()["gemm_positionings"] >= 3
     assert xor_reduce_inplace(out) == c["xor"]
+
+
+@pytest.mark.parametrize("L,n,gap", [(32, (1 << 26) + 777, 0), (32, 1 << 27, 4321), (16, 1 << 27, 0)])
+def test_tensor_core_prefetch_matches_polynomial_jumps(L, n, gap):
+    """VMT_PREFETCH_TENSOR: the next fill's chunk states come from the
+    hand-written tcgen05 kernel (vmt_posmma.cuh) running beside the generation
+    kernel; every fill must equal the jump-positioned reference."""
+    ref = V.VmtGenerator(4242, V.VmtConfig(L))
+    ref.set_tuning(max_chunks=148)
+    ref.set_positioning(1)
+    ref.set_prefetch(0)
+    tc = V.VmtGenerator(4242, V.VmtConfig(L))
+    tc.set_tuning(max_chunks=148)
+    tc.set_prefetch(2)
+    a = torch.empty(n, dtype=torch.uint32, device="cuda")
+    b = torch.empty(n, dtype=torch.uint32, device="cuda")
+    for i in range(8):
+        ref.fill_u32(a)
+        tc.fill_u32(b)
+        torch.cuda.synchronize()
+        assert torch.equal(i32(a), i32(b)), (L, n, i)
+        ref.skip(gap)
+        tc.skip(gap)
+    st = tc.prefetch_stats()
+    if L == 32:  # the 32-lane store kernel leaves room for the GEMM CTA
+        assert st["tensor_prefetches"] >= 3 and st["used"] >= 3, st
+    # a different size next: the prefetched states are discarded, words stay exact
+    m = n // 3
+    a2 = torch.empty(m, dtype=torch.uint32, device="cuda")
+    b2 = torch.empty(m, dtype=torch.uint32, device="cuda")
+    ref.fill_u32(a2)
+    tc.fill_u32(b2)
+    torch.cuda.synchronize()
+    assert torch.equal(i32(a2), i32(b2))
