@@ -487,10 +487,13 @@ def main():
         "per_gpu_value": count / (ms * 1e-3),
         "timing_breakdown_ms": {"gen_kernel": gen_ms, "positioning": jump_ms, "setup_create": setup_ms,
                                 "positioning_gemms": g.positioning_stats()["gemm_positionings"],
-                                "note": "CUDA events on the fill's stream around the chunk positioning (steady "
-                                        "state: one FP4 tensor-core GEMM (int8 fallback) mapping the previous "
-                                        "step's 4736 chunk lane states forward; first fills: polynomial jumps) and the "
-                                        "generation launch of every timed step"},
+                                "prefetch": g.prefetch_stats(),
+                                "note": "CUDA events on the fill's stream around the chunk positioning and the "
+                                        "generation launch of every timed step. Steady state: the next step's 4736 "
+                                        "chunk lane states are computed during this step's generation kernel by the "
+                                        "co-resident tcgen05 FP4 GEMM (vmt_posmma_kernel, on the idle tensor cores), "
+                                        "so 'positioning' is only the wait for it and its cost shows up inside "
+                                        "gen_kernel; first steps: polynomial jumps, then the serial cuBLASLt FP4 GEMM"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": (traffic or {}).get("dram_bytes_per_launch"),
                      "kernel": "vmt_gen_kernel", "peak_source": peak_src,

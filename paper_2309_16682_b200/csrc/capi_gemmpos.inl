@@ -39,18 +39,15 @@ struct GemmPos {
     DevBuf<std::uint8_t> work;
     std::uint64_t scale_rows = 0;
     std::map<std::uint64_t, std::unique_ptr<DevBuf<std::int8_t>>> mats; // delta -> F^(624 delta), word-bit
-    // int8 copies (+ TMA descriptor) for the co-resident tcgen05 prefetch
-    // (vmt_posmma.cuh); the same object as mats[delta] when fp4 == 0
-    struct I8Mat {
-        std::unique_ptr<DevBuf<std::int8_t>> own;
-        const std::int8_t* p = nullptr;
-        CUtensorMap tmap;
-    };
-    std::map<std::uint64_t, I8Mat> mats_i8;
+    // TMA descriptors of the FP4 matrices (B operand of vmt_posmma_kernel)
+    std::map<std::uint64_t, CUtensorMap> tmaps;
+    DevBuf<std::int8_t> pm_a; // FP4 state operand of the co-resident prefetch
+    CUtensorMap pm_tmap_a;
+    const void* pm_tmap_ptr = nullptr;
+    std::uint64_t pm_tmap_rows = 0;
     std::map<std::uint64_t, std::uint64_t> last_use;                     // delta -> tick of its last use
     std::map<std::uint64_t, int> seen;                                   // delta -> transitions observed
     std::uint64_t tick = 0;
-    bool want_i8 = false; // build the int8 copies (co-resident tensor-core prefetch enabled)
     DevBuf<std::int8_t> a;
     DevBuf<std::int32_t> prod;
     bool last_valid = false;
@@ -134,9 +131,9 @@ bool lt_fp4_gemm(GemmPos& gp, const void* mat, const void* bits, float* prod, st
     return ok;
 }
 
-// TMA descriptor of an int8 [19968 out][19968 in] matrix as the B operand of
-// vmt_posmma_kernel: K (in) innermost, boxes of 64 B x 256 rows, 64B swizzle.
-bool make_tmap_b(CUtensorMap& m, const void* base) {
+// TMA descriptor of a K-major FP4 operand [rows][19968 elements = 9984 B]:
+// boxes of 64 B (128 elements) x box_rows rows, 64-byte swizzle.
+bool make_tmap_fp4(CUtensorMap& m, const void* base, std::uint64_t rows, unsigned box_rows) {
     static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
         void* f = nullptr;
         cudaDriverEntryPointQueryResult q{};
@@ -147,9 +144,9 @@ bool make_tmap_b(CUtensorMap& m, const void* base) {
     }();
     if (!enc)
         return false;
-    const cuuint64_t dims[2] = {(cuuint64_t)kWB, (cuuint64_t)kWB};
-    const cuuint64_t strides[1] = {(cuuint64_t)kWB};
-    const cuuint32_t box[2] = {(cuuint32_t)kPmK, 256u};
+    const cuuint64_t dims[2] = {(cuuint64_t)(kWB / 2), (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)(kWB / 2)};
+    const cuuint32_t box[2] = {(cuuint32_t)(kPmKE / 2), box_rows};
     const cuuint32_t estr[2] = {1u, 1u};
     return enc(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -158,44 +155,51 @@ bool make_tmap_b(CUtensorMap& m, const void* base) {
 
 // dst = src jumped by 624*delta words with the co-resident tcgen05 kernel
 // (vmt_posmma.cuh), launched on `st` (a side stream, after the generation
-// kernel). false: no int8 matrix cached for exactly this delta.
+// kernel): the FP4 state operand, then the GEMM. false: no FP4 matrix cached
+// for exactly this delta.
 bool posmma_launch(GemmPos& gp, std::uint64_t delta, const std::uint32_t* src, std::uint32_t* dst, unsigned L,
                    std::uint64_t rows, int sms, cudaStream_t st) {
-    auto it = gp.mats_i8.find(delta);
-    if (it == gp.mats_i8.end() || !gp.mats.count(delta))
+    auto it = gp.tmaps.find(delta);
+    if (gp.fp4 != 1 || it == gp.tmaps.end() || !gp.mats.count(delta))
         return false;
     static bool attr = false;
     if (!attr) {
         VMT_CUDA(cudaFuncSetAttribute(vmt_posmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPmSmem));
         attr = true;
     }
+    const std::uint64_t rows_pad = (rows + kPmM - 1) / kPmM * kPmM;
+    gp.pm_a.reserve(rows_pad * kWB / 2);
+    if (gp.pm_tmap_ptr != gp.pm_a.p || gp.pm_tmap_rows != rows_pad) {
+        if (!make_tmap_fp4(gp.pm_tmap_a, gp.pm_a.p, rows_pad, kPmM))
+            return false;
+        gp.pm_tmap_ptr = gp.pm_a.p;
+        gp.pm_tmap_rows = rows_pad;
+    }
     gp.last_use[delta] = gp.tick;
+    if (rows_pad > rows)
+        VMT_CUDA(cudaMemsetAsync(gp.pm_a.p + rows * kWB / 2, 0, (rows_pad - rows) * kWB / 2, st));
+    const long long nwords = (long long)rows * kN;
+    vmt_states_to_fp4_kernel<<<(unsigned)((nwords + 255) / 256), 256, 0, st>>>(
+        src, (int)L, 0, (int)L, nwords, reinterpret_cast<std::uint8_t*>(gp.pm_a.p));
+    VMT_CUDA(cudaGetLastError());
     PosMmaParams pp;
-    pp.src = src;
     pp.dst = dst;
     pp.L = (int)L;
     pp.rows = (int)rows;
-    pp.m_tiles = (int)((rows + kPmM - 1) / kPmM);
-    static const unsigned flags = std::getenv("VMT_PM_FLAGS") ? (unsigned)std::strtoul(std::getenv("VMT_PM_FLAGS"), nullptr, 0) : 0u;
-    pp.flags = flags;
+    pp.m_tiles = (int)(rows_pad / kPmM);
     const int tiles = pp.m_tiles * kPmNTiles;
-    vmt_posmma_kernel<<<std::min(tiles, sms), kPmThreads, kPmSmem, st>>>(it->second.tmap, pp);
+    vmt_posmma_kernel<<<std::min(tiles, sms), kPmThreads, kPmSmem, st>>>(gp.pm_tmap_a, it->second, pp);
     VMT_CUDA(cudaGetLastError());
     return true;
 }
 
 // p(F) in word-bit coordinates as the GEMM's A operand: FP4 ([out][in], two
 // per byte) or int8.
-void build_gemm_matrix(const Poly& poly, bool fp4, DevBuf<std::int8_t>& m, cudaStream_t st,
-                       DevBuf<std::int8_t>* also_i8 = nullptr) {
+void build_gemm_matrix(const Poly& poly, bool fp4, DevBuf<std::int8_t>& m, cudaStream_t st) {
     DevBuf<std::uint64_t> rows;
     rows.reserve(kMatWords);
     Counters cnt;
     matrix_from_poly(poly, rows.p, st, cnt);
-    if (also_i8) {
-        also_i8->reserve(kGemmMatBytes);
-        vmt_gemm_matrix_kernel<<<dim3((kWB + 255) / 256, kWB), 256, 0, st>>>(rows.p, also_i8->p);
-    }
     if (fp4) {
         m.reserve(kGemmMatBytes / 2);
         vmt_gemm_matrix_fp4_kernel<<<dim3((kWB / 2 + 255) / 256, kWB), 256, 0, st>>>(
@@ -231,23 +235,18 @@ const std::int8_t* gemm_matrix(vmt_generator* h, GemmPos& gp, std::uint64_t delt
             return nullptr;
         VMT_CUDA(cudaStreamSynchronize(st));
         gp.mats.erase(victim);
-        gp.mats_i8.erase(victim);
+        gp.tmaps.erase(victim);
         gp.last_use.erase(victim);
     }
     Gf2Field& F = Gf2Field::instance();
     const unsigned __int128 d = (unsigned __int128)kN * delta;
     std::unique_ptr<DevBuf<std::int8_t>> m(new DevBuf<std::int8_t>());
-    GemmPos::I8Mat i8;
-    if (gp.want_i8 && gp.fp4 == 1)
-        i8.own.reset(new DevBuf<std::int8_t>());
-    build_gemm_matrix(F.x_pow128((std::uint64_t)d, (std::uint64_t)(d >> 64)), gp.fp4 == 1, *m, st, i8.own.get());
+    build_gemm_matrix(F.x_pow128((std::uint64_t)d, (std::uint64_t)(d >> 64)), gp.fp4 == 1, *m, st);
     h->cnt.other += 1;
     const std::int8_t* p = m->p;
-    if (gp.want_i8) {
-        i8.p = i8.own ? i8.own->p : m->p;
-        if (make_tmap_b(i8.tmap, i8.p))
-            gp.mats_i8[delta] = std::move(i8);
-    }
+    CUtensorMap tm;
+    if (gp.fp4 == 1 && make_tmap_fp4(tm, p, kWB, kPmNH))
+        gp.tmaps[delta] = tm;
     gp.mats[delta] = std::move(m);
     gp.last_use[delta] = gp.tick;
     return p;
@@ -326,7 +325,7 @@ bool gemm_position_exact(vmt_generator* h, GemmPos& gp, const std::uint32_t* src
         VMT_CUDA(cudaStreamSynchronize(st));
         gp.fp4 = 0;
         gp.mats.clear();
-        gp.mats_i8.clear();
+        gp.tmaps.clear();
         gp.last_use.clear();
     }
     const std::int8_t* mat = gemm_matrix(h, gp, delta, st);

@@ -130,8 +130,6 @@ int prepare_gen(int dev, GenFn fn, int nt, int smem) {
     const void* key = reinterpret_cast<const void*>(fn);
     if (!d.smem_set.count(key)) {
         VMT_CUDA(cudaFuncSetAttribute(key, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        if (std::getenv("VMT_FORCE_CARVEOUT")) // experiment knob
-            VMT_CUDA(cudaFuncSetAttribute(key, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         int occ = 0;
         VMT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, key, nt, smem));
         d.occ[key] = std::max(occ, 1);
@@ -405,6 +403,16 @@ void launch_jumps_affine(cudaStream_t st, const std::uint32_t* src, int src_stri
 
 namespace {
 struct GemmPos; // capi_gemmpos.inl
+
+// Prefetch mode of new generators (vmt_set_prefetch); env VMT_PREFETCH overrides.
+int default_prefetch() {
+    static const int v = [] {
+        const char* e = std::getenv("VMT_PREFETCH");
+        const int m = e ? std::atoi(e) : VMT_PREFETCH_TENSOR;
+        return (m >= VMT_PREFETCH_OFF && m <= VMT_PREFETCH_TENSOR) ? m : VMT_PREFETCH_TENSOR;
+    }();
+    return v;
+}
 }
 
 // ------------------------------------------------------------------ handle --
@@ -426,7 +434,7 @@ struct vmt_generator {
 
     DevBuf<std::uint32_t> chunks;    // [C][624][L]
     DevBuf<std::uint32_t> chunks_alt; // prefetched chunk states of the predicted next fill
-    int prefetch = VMT_PREFETCH_OFF; // position the predicted next fill while this one generates
+    int prefetch = default_prefetch(); // position the predicted next fill while this one generates
     bool pref_valid = false;
     bool pref_inflight = false;      // ev_pref recorded and not yet waited for by a fill
     std::uint64_t pref_b0 = 0, pref_B = 0, pref_C = 0;
@@ -735,10 +743,8 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
         h->cnt.pref_used += 1;
     }
     if (!positioned && h->positioning != 1 && C * h->L >= gemm_min_rows()) {
-        if (!h->gemm) {
+        if (!h->gemm)
             h->gemm = new GemmPos();
-            h->gemm->want_i8 = h->prefetch == VMT_PREFETCH_TENSOR;
-        }
         GemmPos& gp = *h->gemm;
         if (gp.last_valid && gp.last_B == B && gp.last_C == C && b0 > gp.last_b0) {
             const std::uint64_t delta = b0 - gp.last_b0;
@@ -855,6 +861,7 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
             h->pref_B = B;
             h->pref_C = C;
             h->cnt.tc_prefetches += 1;
+            h->cnt.other += 2; // FP4 state operand + vmt_posmma_kernel
         }
         prefetch_now = false;
     }
@@ -1460,8 +1467,6 @@ int vmt_set_prefetch(vmt_handle h, int enable) {
         require(enable >= VMT_PREFETCH_OFF && enable <= VMT_PREFETCH_TENSOR, VMT_EINVAL, "unknown prefetch mode");
         h->prefetch = enable;
         h->pref_valid = false;
-        if (h->gemm)
-            h->gemm->want_i8 = enable == VMT_PREFETCH_TENSOR;
     });
 }
 

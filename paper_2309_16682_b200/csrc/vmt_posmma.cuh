@@ -9,23 +9,26 @@
 // runs: the generation CTA (one per SM, 108 KB of shared memory, 168
 // registers x 256 threads) leaves ~120 KB of shared memory, 22.5k registers
 // and the whole tensor core of every SM idle, and one CTA of this kernel
-// (192 threads, 80 KB) fits beside it. The positioning then costs the
-// generation kernel only the issue slots of the operand expansion instead of
-// a serial 0.8 ms GEMM between fills.
+// (192 threads, 103 KB) fits beside it.
 //
-// Tile: 128 lane states (M) x 512 output bit columns (N, two N=256
-// accumulators = all 512 TMEM columns), K staged 64 bytes at a time through a
-// 2-deep ring. kind::i8 with 0/1 operands and s32 accumulation is exact
-// (sums <= 19937); bit j of the new state is the low bit of column j.
-//   warp 0     TMA producer: B = M[j][i] int8, K-major, 64B-swizzled boxes
+// What it costs the generation kernel is mostly shared-memory bandwidth: the
+// tensor core reads its operands from shared memory, (1/M + 1/N) bytes per
+// MAC per byte-wide element, and the generation kernel's ring traffic runs
+// through the same ports (measured with an int8 version: ~0.8 ms added to an
+// 11.2 ms generation kernel, all of it the MMA operand reads). So the
+// operands are FP4 (kind::mxf4: e2m1 0/1 values, unit ue8m0 block scales held
+// in TMEM, fp32 accumulation -- exact, sums <= 19937), half the bytes of int8.
+//
+// Tile: 128 lane states (M) x 416 output bit columns (two N=208 MMAs side by
+// side in TMEM = 13 whole state words), K staged 128 elements (64 bytes) at
+// a time through a 3-deep ring, both operands by TMA (64-byte swizzle, L2
+// evict_last so the CTAs on the same N slice share B through L2):
+//   warp 0     TMA producer: A = the states' FP4 operand [rows][9984 B]
+//              (vmt_states_to_fp4_kernel), B = F^(624D) FP4 [19968][9984 B]
 //   warp 1     TMEM allocator; one elected lane issues tcgen05.mma
-//   warps 2-5  A producers: expand the compact state words of their 32 rows
-//              into 0/1 bytes in the 64B-swizzled K-major layout (no operand
-//              buffer in HBM); then the epilogue of the same rows: tcgen05.ld
-//              32 columns = one state word per load, packed to bits, stored
+//   warps 2-5  unit scale factors into TMEM; epilogue: tcgen05.ld 32 columns
+//              = one state word per load, parity of each sum -> bit, stored
 //              into the interleaved [C][624][L] chunk-state array.
-// Tiles are ordered N-slice-major so the CTAs running at the same time share
-// B slices through L2; the 12 MB of compact states stay L2-resident.
 #pragma once
 
 #include <cuda.h>
@@ -36,52 +39,25 @@
 namespace vmt_b200 {
 
 constexpr int kPmM = 128;                  // lane states per tile
-constexpr int kPmN = 512;                  // output bit columns per tile
-constexpr int kPmK = 64;                   // K bytes per stage (= one 64B swizzle atom row)
-constexpr int kPmStages = 2;
-constexpr int kPmABytes = kPmM * kPmK;     // 8 KB
-constexpr int kPmBBytes = kPmN * kPmK;     // 32 KB (two 256-row TMA boxes)
-constexpr int kPmStageBytes = kPmABytes + kPmBBytes;
-constexpr int kPmKSteps = (kN * 32) / kPmK; // 312
-constexpr int kPmNTiles = (kN * 32) / kPmN; // 39
+constexpr int kPmNH = 208;                 // output bit columns per MMA (N)
+constexpr int kPmN = 2 * kPmNH;            // per tile: two MMAs side by side in TMEM = 13 state words
+constexpr int kPmKE = 128;                 // K elements (input bits) per stage = 64 bytes of FP4
+constexpr int kPmStages = 3;
+constexpr int kPmABytes = kPmM * kPmKE / 2;        // 8 KB
+constexpr int kPmBHBytes = kPmNH * kPmKE / 2;      // 13 KB per N half
+constexpr int kPmStageBytes = kPmABytes + 2 * kPmBHBytes;
+constexpr int kPmKSteps = (kN * 32) / kPmKE; // 156
+constexpr int kPmNTiles = (kN * 32) / kPmN;  // 48
 constexpr int kPmThreads = 192;
 constexpr int kPmSmem = kPmStages * kPmStageBytes + 1024 /* align */ + 128 /* barriers */;
+constexpr int kPmSfCol = 448;              // TMEM columns [448, 512): unit scale factors
 
 struct PosMmaParams {
-    const std::uint32_t* src; // [C][624][L] chunk lane states (this fill's)
     std::uint32_t* dst;       // [C][624][L] jumped by the matrix (the next fill's)
     int L;
     int rows;                 // C * L
     int m_tiles;              // ceil(rows / 128)
-    unsigned flags;           // experiment knobs (VMT_PM_FLAGS): bit0 polite waits, bit1 no A expansion,
-                              // bit2 no MMA, bits 8..23 MMA pacing in 64 ns units per stage
 };
-
-// Waits without competing for issue slots with the co-resident generation
-// warps: a suspending try_wait, then exponential __nanosleep backoff.
-__device__ __forceinline__ void mbar_wait_polite(unsigned long long* bar, unsigned parity) {
-    unsigned ns = 32;
-    for (;;) {
-        unsigned done;
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 100000;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-        if (done)
-            return;
-        __nanosleep(ns);
-        ns = ns < 2048 ? ns * 2 : ns;
-    }
-}
-__device__ __forceinline__ void pm_wait(unsigned long long* bar, unsigned parity, unsigned flags) {
-    if (flags & 1u)
-        mbar_wait_polite(bar, parity);
-    else
-        mbar_wait_parity(bar, parity);
-}
 
 // ---- tcgen05 / TMA primitives -------------------------------------------------
 __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
@@ -112,13 +88,17 @@ __device__ __forceinline__ void tc_commit(unsigned long long* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
 }
-__device__ __forceinline__ void tc_mma_i8(unsigned tmem_d, unsigned long long adesc, unsigned long long bdesc,
-                                          unsigned idesc, unsigned accumulate) {
+// D[tmem] (+)= A[smem] x B[smem]^T, FP4 e2m1 operands with per-32-element
+// ue8m0 scale factors read from TMEM (all 1.0 here), fp32 accumulation
+__device__ __forceinline__ void tc_mma_mxf4(unsigned tmem_d, unsigned long long adesc, unsigned long long bdesc,
+                                            unsigned idesc, unsigned tmem_sfa, unsigned tmem_sfb,
+                                            unsigned accumulate) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%4], [%5], p;\n\t}" ::"r"(
+            tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(tmem_sfa), "r"(tmem_sfb), "r"(accumulate)
         : "memory");
 }
 // K-major operand in the 64-byte swizzle layout: 8-row groups of 8 x 64 B
@@ -132,35 +112,33 @@ __device__ __forceinline__ unsigned long long sw64_desc(unsigned saddr) {
     d |= (unsigned long long)4 << 61;                     // SWIZZLE_64B
     return d;
 }
-// kind::i8 instruction descriptor: s32 accumulator, u8 x u8, both K-major,
-// N = 256, M = 128
-constexpr unsigned kPmIdesc = (2u << 4) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
-
-// 32 bits -> 32 bytes of 0/1, as 8 u32 (byte b = bit b)
-__device__ __forceinline__ void expand_bits(std::uint32_t w, std::uint32_t q[8]) {
-#pragma unroll
-    for (int n = 0; n < 8; ++n)
-        q[n] = (((w >> (4 * n)) & 15u) * 0x00204081u) & 0x01010101u;
-}
+// kind::mxf4 instruction descriptor: A and B e2m1 (MXF4 format 1), both
+// K-major, N = 208, ue8m0 scales, M = 128, K = 64, scale-factor ids 0
+constexpr unsigned kPmIdesc = (1u << 7) | (1u << 10) | ((unsigned)(kPmNH >> 3) << 17) | (1u << 23) |
+                              ((128u >> 4) << 24);
 
 __global__ void __launch_bounds__(kPmThreads, 1)
-    vmt_posmma_kernel(const __grid_constant__ CUtensorMap tmap_b, const PosMmaParams p) {
+    vmt_posmma_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                      const PosMmaParams p) {
     extern __shared__ unsigned char pm_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(pm_raw) + 1023) &
                                                            ~static_cast<std::uintptr_t>(1023));
     unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + kPmStages * kPmStageBytes);
     unsigned long long* empty = full + kPmStages;
-    unsigned long long* accf = empty + kPmStages;
-    unsigned* tmem_slot = reinterpret_cast<unsigned*>(accf + 1);
+    unsigned long long* accf = empty + kPmStages; // MMA -> epilogue: accumulators complete
+    unsigned long long* accd = accf + 1;           // epilogue -> MMA: accumulators drained
+    unsigned* tmem_slot = reinterpret_cast<unsigned*>(accd + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kPmStages; ++s) {
-            mbar_init(&full[s], 5); // 4 A-producer warps + the TMA producer's expect_tx
+            mbar_init(&full[s], 1); // the TMA producer's expect_tx (A + B bytes)
             mbar_init(&empty[s], 1);
         }
         mbar_init(accf, 1);
+        mbar_init(accd, 4);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&tmap_a)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&tmap_b)) : "memory");
     }
     if (warp == 1) {
@@ -172,6 +150,23 @@ __global__ void __launch_bounds__(kPmThreads, 1)
     __syncthreads();
     tc_fence_after();
     const unsigned tmem = *tmem_slot;
+    if (warp >= 2) {
+        // unit scale factors (ue8m0 0x7F = 1.0) in every byte of TMEM columns
+        // [448, 512) of this warp's lane quarter: whatever the scale-factor
+        // layout inside that range, every factor reads as 1.0
+        const unsigned one4 = 0x7F7F7F7Fu;
+#pragma unroll
+        for (int c0 = kPmSfCol; c0 < 512; c0 += 16)
+            asm volatile(
+                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                    tmem + ((unsigned)((warp & 3) * 32) << 16) + (unsigned)c0),
+                "r"(one4)
+                : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
 
     const int ntiles = p.m_tiles * kPmNTiles;
     if (warp == 0) {
@@ -179,39 +174,42 @@ __global__ void __launch_bounds__(kPmThreads, 1)
             const unsigned long long pol = l2_policy_evict_last();
             unsigned it = 0;
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                const int n = tile / p.m_tiles;
+                const int n = tile / p.m_tiles, m = tile % p.m_tiles;
                 for (int ks = 0; ks < kPmKSteps; ++ks, ++it) {
                     const int s = it % kPmStages;
                     const unsigned u = it / kPmStages;
                     if (u > 0)
-                        pm_wait(&empty[s], (u - 1) & 1, p.flags);
-                    unsigned char* b = smem + s * kPmStageBytes + kPmABytes;
-                    mbar_arrive_expect_tx(&full[s], kPmBBytes);
-                    tma_load_2d(b, &tmap_b, ks * kPmK, n * kPmN, &full[s], pol);
-                    tma_load_2d(b + kPmBBytes / 2, &tmap_b, ks * kPmK, n * kPmN + 256, &full[s], pol);
+                        mbar_wait_parity(&empty[s], (u - 1) & 1);
+                    unsigned char* a = smem + s * kPmStageBytes;
+                    unsigned char* b = a + kPmABytes;
+                    mbar_arrive_expect_tx(&full[s], kPmStageBytes);
+                    tma_load_2d(a, &tmap_a, ks * (kPmKE / 2), m * kPmM, &full[s], pol);
+                    tma_load_2d(b, &tmap_b, ks * (kPmKE / 2), n * kPmN, &full[s], pol);
+                    tma_load_2d(b + kPmBHBytes, &tmap_b, ks * (kPmKE / 2), n * kPmN + kPmNH, &full[s], pol);
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            unsigned it = 0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            unsigned it = 0, tcount = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tcount) {
+                if (tcount > 0) { // the previous tile's epilogue has read the accumulators
+                    mbar_wait_parity(accd, (tcount - 1) & 1);
+                    tc_fence_after();
+                }
                 for (int ks = 0; ks < kPmKSteps; ++ks, ++it) {
                     const int s = it % kPmStages;
-                    pm_wait(&full[s], (it / kPmStages) & 1, p.flags);
+                    mbar_wait_parity(&full[s], (it / kPmStages) & 1);
                     tc_fence_after();
                     const unsigned a = smem_u32(smem + s * kPmStageBytes);
                     const unsigned b = a + kPmABytes;
-                    if (p.flags >> 8)
-                        __nanosleep(64u * ((p.flags >> 8) & 0xFFFFu));
-                    if (!(p.flags & 4u))
 #pragma unroll
-                    for (int kk = 0; kk < kPmK / 32; ++kk) {
+                    for (int kk = 0; kk < 2; ++kk) { // two K=64 MMAs (32 bytes each) per stage
 #pragma unroll
                         for (int h = 0; h < 2; ++h)
-                            tc_mma_i8(tmem + 256 * h, sw64_desc(a + 32 * kk),
-                                      sw64_desc(b + h * (kPmBBytes / 2) + 32 * kk), kPmIdesc,
-                                      (ks | kk) != 0);
+                            tc_mma_mxf4(tmem + kPmNH * h, sw64_desc(a + 32 * kk),
+                                        sw64_desc(b + h * kPmBHBytes + 32 * kk), kPmIdesc, tmem + kPmSfCol,
+                                        tmem + kPmSfCol + 32, (ks | kk) != 0);
                     }
                     tc_commit(&empty[s]); // frees the stage when these MMAs are done
                 }
@@ -219,47 +217,17 @@ __global__ void __launch_bounds__(kPmThreads, 1)
             }
         }
     } else {
-        // A producers + epilogue: TMEM lane quarter (warp % 4) = rows 32*(warp%4) + lane
+        // epilogue: TMEM lane quarter (warp % 4) = rows 32*(warp%4) + lane
         const int rq = (warp & 3) * 32;
         const int r = rq + lane; // row within the tile
-        unsigned it = 0, tcount = 0;
+        unsigned tcount = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tcount) {
             const int n = tile / p.m_tiles, m = tile % p.m_tiles;
             const int row = m * kPmM + r;
             const bool valid = row < p.rows;
             const int c = valid ? row / p.L : 0, t = valid ? row % p.L : 0;
-            const std::uint32_t* src = p.src + (long long)c * kN * p.L + t;
-            unsigned char* arow = smem + (r >> 3) * 512 + (r & 7) * 64;
-            const int sw = (r >> 1) & 3;
-            for (int ks = 0; ks < kPmKSteps; ++ks, ++it) {
-                const int s = it % kPmStages;
-                const unsigned u = it / kPmStages;
-                std::uint32_t w0 = 0, w1 = 0;
-                if (valid) {
-                    w0 = __ldg(src + (long long)(2 * ks) * p.L);
-                    w1 = __ldg(src + (long long)(2 * ks + 1) * p.L);
-                    if (ks == 0)
-                        w0 &= kUpperMask;
-                }
-                if (u > 0)
-                    pm_wait(&empty[s], (u - 1) & 1, p.flags);
-                unsigned char* a = arow + s * kPmStageBytes;
-                std::uint32_t q[8];
-                if (!(p.flags & 2u)) {
-                expand_bits(w0, q);
-                *reinterpret_cast<uint4*>(a + 16 * (0 ^ sw)) = make_uint4(q[0], q[1], q[2], q[3]);
-                *reinterpret_cast<uint4*>(a + 16 * (1 ^ sw)) = make_uint4(q[4], q[5], q[6], q[7]);
-                expand_bits(w1, q);
-                *reinterpret_cast<uint4*>(a + 16 * (2 ^ sw)) = make_uint4(q[0], q[1], q[2], q[3]);
-                *reinterpret_cast<uint4*>(a + 16 * (3 ^ sw)) = make_uint4(q[4], q[5], q[6], q[7]);
-                }
-                fence_proxy_async_smem(); // generic-proxy writes -> visible to the tensor core
-                __syncwarp();
-                if (lane == 0)
-                    mbar_arrive(&full[s]);
-            }
-            // epilogue: 16 state words (512 columns) of this row
-            pm_wait(accf, tcount & 1, p.flags);
+            // 13 state words (416 columns) of this row
+            mbar_wait_parity(accf, tcount & 1);
             tc_fence_after();
             std::uint32_t* dst = p.dst + (long long)c * kN * p.L + t;
 #pragma unroll 1
@@ -277,13 +245,16 @@ __global__ void __launch_bounds__(kPmThreads, 1)
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 std::uint32_t w = 0;
 #pragma unroll
-                for (int b = 0; b < 32; ++b)
-                    w |= (v[b] & 1u) << b;
+                for (int b = 0; b < 32; ++b) // exact fp32 sums of 0/1 products: bit = parity
+                    w |= ((std::uint32_t)__float2int_rn(__uint_as_float(v[b])) & 1u) << b;
                 const int k = n * (kPmN / 32) + j;
                 if (valid)
                     dst[(long long)k * p.L] = k == 0 ? (w & kUpperMask) : w;
             }
             tc_fence_before(); // TMEM reads ordered before the next tile's MMAs
+            __syncwarp();
+            if (lane == 0)
+                mbar_arrive(accd); // this warp's rows are drained
         }
     }
     tc_fence_before();

@@ -28,6 +28,7 @@ def test_gemm_positioning_matches_polynomial_jumps(L, n, gap):
     gem = V.VmtGenerator(5489, V.VmtConfig(L))
     gem.set_tuning(max_chunks=148)
     gem.set_positioning(0)
+    gem.set_prefetch(0)  # serial GEMM path (the prefetch has its own test)
     a = torch.empty(n, dtype=torch.uint32, device="cuda")
     b = torch.empty(n, dtype=torch.uint32, device="cuda")
     for i in range(6):
@@ -52,6 +53,7 @@ def test_gemm_positioning_mode2_and_shape_changes():
         g.set_tuning(max_chunks=148)
     ref.set_positioning(1)
     gem.set_positioning(2)
+    gem.set_prefetch(0)  # serial GEMM path (the prefetch has its own test)
     plan = [n, n, n, n // 2, n, n]
     for i, m in enumerate(plan):
         a = torch.empty(m, dtype=torch.uint32, device="cuda")
@@ -79,7 +81,7 @@ import paper_2309_16682_b200 as V
 n = (1 << 25) + 5
 ref = V.VmtGenerator(9, V.VmtConfig(16)); gem = V.VmtGenerator(9, V.VmtConfig(16))
 for g in (ref, gem): g.set_tuning(max_chunks=148)
-ref.set_positioning(1); gem.set_positioning(2)
+ref.set_positioning(1); gem.set_positioning(2); gem.set_prefetch(0)
 a = torch.empty(n, dtype=torch.uint32, device="cuda"); b = torch.empty(n, dtype=torch.uint32, device="cuda")
 for i in range(4):
     ref.fill_u32(a); gem.fill_u32(b); torch.cuda.synchronize()
@@ -103,6 +105,7 @@ def test_gemm_positioning_in_fused_modes():
         g.set_tuning(max_chunks=148)
     ref.set_positioning(1)
     gem.set_positioning(2)
+    gem.set_prefetch(0)  # serial GEMM path (the prefetch has its own test)
     for _ in range(3):
         assert ref.checksum_xor(n) == gem.checksum_xor(n)
     for _ in range(3):
@@ -130,6 +133,7 @@ def test_gemm_positioning_reuses_matrix_with_block_advance():
         g.set_tuning(max_chunks=148)
     ref.set_positioning(1)
     gem.set_positioning(2)
+    gem.set_prefetch(0)  # serial GEMM path (the prefetch has its own test)
     for k in range(10):
         n = bw * (3000 + (k % 3))
         a = torch.empty(n, dtype=torch.uint32, device="cuda")
@@ -150,12 +154,14 @@ def test_gemm_positioned_stream_pinned_to_oracle(golden):
     c = golden["c4_full"]
     g = V.VmtGenerator(c["seed"], V.VmtConfig(c["lanes"]))
     g.set_positioning(2)
+    g.set_prefetch(0)  # serial GEMM path (the prefetch has its own test)
     x = 0
     for _ in range(4):
         x ^= g.checksum_xor(1 << 32)
     assert x == c["xor"] and g.positioning_stats()["gemm_positionings"] >= 2
     g = V.VmtGenerator(c["seed"], V.VmtConfig(c["lanes"]))
     g.set_positioning(2)
+    g.set_prefetch(0)  # serial GEMM path (the prefetch has its own test)
     out = torch.empty(c["count"], dtype=torch.uint32, device="cuda")
     for k in range(4):
         g.fill_u32(out[k << 32:(k + 1) << 32])
