@@ -853,7 +853,17 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
         // the generation CTAs leave free on every SM
         h->chunks_alt.reserve((size_t)C * kN * h->L);
         VMT_CUDA(cudaStreamWaitEvent(h->side, h->ev_chunks, 0));
-        if (posmma_launch(*h->gemm, next_b0 - b0, h->chunks.p, h->chunks_alt.p, h->L, C * h->L, sms, h->side)) {
+        // a cached matrix for the delta or for a base at most 4 blocks below it
+        // (the rest regenerated in place, as in gemm_position)
+        const std::uint64_t delta = next_b0 - b0, base = usable_base(*h->gemm, delta);
+        if (base && posmma_launch(*h->gemm, base, h->chunks.p, h->chunks_alt.p, h->L, C * h->L, sms, h->side)) {
+            if (delta > base) {
+                vmt_advance_blocks_kernel<<<(unsigned)((C * h->L + kAdvWarps - 1) / kAdvWarps), 32 * kAdvWarps, 0,
+                                            h->side>>>(h->chunks_alt.p, (int)h->L, (long long)(C * h->L),
+                                                       (int)(delta - base));
+                VMT_CUDA(cudaGetLastError());
+                h->cnt.other += 1;
+            }
             VMT_CUDA(cudaEventRecord(h->ev_pref, h->side));
             h->pref_valid = true;
             h->pref_inflight = true;
@@ -1377,7 +1387,9 @@ int vmt_jump_states(const uint32_t* src, uint64_t n, const uint64_t* distances, 
         DevBuf<long long> js, jd;
         DevBuf<int> jp;
         Counters cnt;
-        for (int j = 0; j < 8; ++j) {
+        // digits 2..7 (bits 16..63) by table jumps, bits 0..15 by direct
+        // advance (vmt_advance_steps_kernel): F^d = F^(d_hi) F^(d_lo)
+        for (int j = 2; j < 8; ++j) {
             std::vector<long long> vs, vd;
             std::vector<int> vp;
             for (std::uint64_t i = 0; i < n; ++i) {
@@ -1391,6 +1403,12 @@ int vmt_jump_states(const uint32_t* src, uint64_t n, const uint64_t* distances, 
             // in place: each warp reads its whole state before writing it
             launch_jumps(st, buf.p, 1, buf.p, 1, tables, vs, vd, vp, js, jd, jp, cnt);
         }
+        DevBuf<unsigned long long> dd;
+        dd.reserve(n);
+        VMT_CUDA(cudaMemcpyAsync(dd.p, d.data(), n * 8, cudaMemcpyHostToDevice, st));
+        vmt_advance_steps_kernel<<<(unsigned)((n + kStepWarps - 1) / kStepWarps), 32 * kStepWarps, 0, st>>>(
+            buf.p, (long long)n, dd.p, 0xFFFFu);
+        VMT_CUDA(cudaGetLastError());
         if (is_device_ptr(dst))
             VMT_CUDA(cudaMemcpyAsync(dst, buf.p, n * kN * 4, cudaMemcpyDeviceToDevice, st));
         else

@@ -6,6 +6,9 @@
   jump  : vmt_jump_kernel, the bench's positioning launch (147 x 32 = 4704 jobs)
   stats : vmt_gen_kernel MODE_STATS (fused monobit + byte histogram), 2^32 words
   xor   : vmt_gen_kernel MODE_XOR (fused checksum), 2^32 words
+  posmma: vmt_posmma_kernel, the co-resident tcgen05 FP4 positioning GEMM
+          (4736 lane states x F^(624 D)); under ncu it runs serialised, i.e.
+          alone on the GPU (6 fills of 2^32 words; it launches from fill 3 on)
 Each target runs its call three times; profile with --launch-skip/-c on the
 kernel name (see profiles/scripts/profile.sh).
 """
@@ -27,6 +30,12 @@ if what in ("gen", "jump"):
 elif what == "stats":
     for _ in range(3):
         g.stat_counts(n)
+elif what == "posmma":
+    g.set_prefetch(2)
+    buf = torch.empty(n, dtype=torch.uint32, device="cuda")
+    for _ in range(6):
+        g.fill_u32(buf)
+    assert g.prefetch_stats()["tensor_prefetches"] >= 2, g.prefetch_stats()
 elif what == "xor":
     for _ in range(3):
         g.checksum_xor(n)

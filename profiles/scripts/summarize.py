@@ -24,6 +24,8 @@ METRICS = [
     ("smsp__inst_executed.sum", "warp instructions"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
     ("sm__cycles_elapsed.avg.per_second", "SM clock"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe %"),
+    ("lts__t_bytes.sum", "L2 bytes"),
 ]
 
 
@@ -46,7 +48,7 @@ def to_bytes(val, unit):
     return f * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
 
 
-for name in ("gen", "xor", "stats", "jump"):
+for name in ("gen", "xor", "stats", "jump", "posmma"):
     m, h, v = raw(f"{OUT}/prof_{name}.ncu-rep")
     print(f"\n### {name}: {m['Kernel Name'][0] if 'Kernel Name' in m else ''}")
     for key, label in METRICS:

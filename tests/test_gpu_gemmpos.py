@@ -169,7 +169,8 @@ def test_gemm_positioned_stream_pinned_to_oracle(golden):
     assert xor_reduce_inplace(out) == c["xor"]
 
 
-@pytest.mark.parametrize("L,n,gap", [(32, (1 << 26) + 777, 0), (32, 1 << 27, 4321), (16, 1 << 27, 0)])
+@pytest.mark.parametrize("L,n,gap", [(32, (1 << 26) + 777, 0), (32, 1 << 27, 4321), (16, 1 << 27, 0),
+                                     (32, 1 << 32, 0)])
 def test_tensor_core_prefetch_matches_polynomial_jumps(L, n, gap):
     """VMT_PREFETCH_TENSOR: the next fill's chunk states come from the
     hand-written tcgen05 kernel (vmt_posmma.cuh) running beside the generation
@@ -192,7 +193,9 @@ def test_tensor_core_prefetch_matches_polynomial_jumps(L, n, gap):
         tc.skip(gap)
     st = tc.prefetch_stats()
     if L == 32:  # the 32-lane store kernel leaves room for the GEMM CTA
-        assert st["tensor_prefetches"] >= 3 and st["used"] >= 3, st
+        # (2^32 words = 215092.5 blocks: the block delta alternates, one
+        # cached matrix + in-place regeneration serves both)
+        assert st["tensor_prefetches"] >= 4 and st["used"] >= 4, st
     # a different size next: the prefetched states are discarded, words stay exact
     m = n // 3
     a2 = torch.empty(m, dtype=torch.uint32, device="cuda")

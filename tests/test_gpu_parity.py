@@ -226,6 +226,20 @@ def test_jump_states_config5(gnpz, oracle):
         assert np.array_equal(out[i], j)
 
 
+def test_jump_states_small_and_edge_distances(oracle):
+    """Distances whose low 16 bits are applied by direct advance
+    (vmt_advance_steps_kernel) and whose high bits by table jumps: every
+    state word equals the oracle's polynomial jump, word 0 included."""
+    seeds = np.arange(11, 11 + 12, dtype=np.uint32)
+    st = V.seed_states(seeds)
+    d = np.array([0, 1, 226, 227, 623, 624, 625, 65535, 65536, 65537, (1 << 40) + 12345, (1 << 64) - 1],
+                 dtype=np.uint64)
+    out = V.jump_states(st, d)
+    for i in range(len(d)):
+        j = oracle.poly_jump(st[i], oracle.x_pow_mod(int(d[i])))
+        assert np.array_equal(out[i], j), int(d[i])
+
+
 def test_create_from_states_roundtrip(oracle):
     lanes = oracle.dephased_states(7, 8, oracle.x_pow2_mod(12))
     g = V.VmtGenerator(0, lane_states=lanes)
