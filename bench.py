@@ -287,7 +287,7 @@ def extras(dev) -> dict:
     jumped = torch.empty_like(states)
     s = timed(lambda: V.jump_states(states, dists, out=jumped), reps=2)
     out["c5_4096_jumps_64bit"] = {"value": 4096 / s, "unit": "state jumps/s", "ms": s * 1e3,
-                                  "note": "8 digit-table polynomial jumps per state (64-bit distance)"}
+                                  "note": "6 digit-table polynomial jumps per state (bits 16..63 of the 64-bit distance) + a direct advance by the low 16 bits"}
     # fused statistics consumer (monobit + chi2 byte histogram), 2^32 words, nothing stored
     n = 1 << 32
     g = V.VmtGenerator(5489, V.VmtConfig(32))
@@ -459,6 +459,21 @@ def main():
         e2e_s = max_over_ranks(e2e_s, coll)
         e2e = {"value": T / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": T * 4,
                "ms_per_step": e2e_s * 1e3, "host_buffer": kind, "steps": args.e2e_steps}
+        # the link the e2e number is bound by: a plain 1 GiB pinned D2H copy
+        if kind == "pinned":
+            src = torch.empty(1 << 28, dtype=torch.uint32, device=dev)
+            best = 0.0
+            for _ in range(3):
+                torch.cuda.synchronize()
+                t1 = time.perf_counter()
+                host[: 1 << 28].copy_(src, non_blocking=True)
+                torch.cuda.synchronize()
+                best = max(best, (1 << 30) / (time.perf_counter() - t1) / 1e9)
+            e2e["link_probe"] = {"d2h_memcpy_gbs": best, "e2e_gbs": T * 4 / e2e_s / 1e9 / world,
+                                 "frac": T * 4 / e2e_s / 1e9 / world / best,
+                                 "note": "pinned 1 GiB cudaMemcpy D2H (PCIe): the e2e fill moves 4 B per word "
+                                         "over the same link"}
+            del src
         del host
 
     peak, peak_src = measured_peak()
