@@ -414,6 +414,31 @@ def main():
     gen_ms = max_over_ranks(gen_tot / max(fills, 1), coll)
     jump_ms = max_over_ranks(jump_tot / max(fills, 1), coll)
 
+    # -- the same steps with the serial positioning (no co-resident tcgen05
+    # prefetch): explains the split between the generation kernel's own
+    # roofline and the positioning it hides (reported, not the headline)
+    serial = None
+    if args.mode == "store" and not args.no_extras:
+        g.set_prefetch(0)
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize(dev)
+        g.set_profiling(True)
+        g.profile_totals()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(3):
+            step()
+        f1.record(stream)
+        f1.synchronize()
+        sf, sj, sg = g.profile_totals()
+        g.set_profiling(False)
+        g.set_prefetch(2)
+        serial = {"ms_per_step": f0.elapsed_time(f1) / 3, "gen_kernel": sg / max(sf, 1),
+                  "positioning": sj / max(sf, 1),
+                  "gen_roofline_frac": count * 4 / (sg / max(sf, 1) * 1e-3) / 1e9 / measured_peak()[0],
+                  "note": "3 steps with vmt_set_prefetch(OFF): one cuBLASLt FP4 GEMM between steps instead"}
+
     # -- global checksum of one full 2^34 range (config 4 verification)
     g.seek(start)
     csum = combine_xor(g.checksum_xor(count), coll)
@@ -503,6 +528,7 @@ def main():
         "timing_breakdown_ms": {"gen_kernel": gen_ms, "positioning": jump_ms, "setup_create": setup_ms,
                                 "positioning_gemms": g.positioning_stats()["gemm_positionings"],
                                 "prefetch": g.prefetch_stats(),
+                                "serial_positioning": serial,
                                 "note": "CUDA events on the fill's stream around the chunk positioning and the "
                                         "generation launch of every timed step. Steady state: the next step's 4736 "
                                         "chunk lane states are computed during this step's generation kernel by the "
