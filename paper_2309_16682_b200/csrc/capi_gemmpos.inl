@@ -274,8 +274,16 @@ bool gemm_position_exact(vmt_generator* h, GemmPos& gp, const std::uint32_t* src
 bool gemm_position(vmt_generator* h, GemmPos& gp, const std::uint32_t* src, std::uint32_t* dst, std::uint64_t rows,
                    std::uint64_t delta, cudaStream_t st) {
     std::uint64_t base = usable_base(gp, delta);
-    if (base == 0)
+    if (base == 0) {
+        // no matrix yet: build it for the smallest recently seen delta in
+        // [delta-4, delta], so that the alternating neighbour reuses it
         base = delta;
+        for (std::uint64_t k = 4; k >= 1; --k)
+            if (k < delta && gp.seen.count(delta - k)) {
+                base = delta - k;
+                break;
+            }
+    }
     if (!gemm_position_exact(h, gp, src, dst, rows, base, st))
         return false;
     if (delta > base) {

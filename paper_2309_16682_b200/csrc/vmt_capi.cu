@@ -636,8 +636,8 @@ cudaEvent_t* prof_next(vmt_generator* h) {
 //
 // Fused XOR fills (no stores) run at ~5.5e8 words/s per lane and saturate at
 // ~3.4e12 words/s per GPU; and when the previous fill had the same size the
-// positioning is one GEMM (capi_gemmpos.inl, ~0.12 ms + 0.14 us per lane
-// state) rather than jumps.
+// positioning is one FP4 GEMM (capi_gemmpos.inl, measured ~0.03 ms + 0.165 us
+// per lane state: 1024 rows 0.21 ms, 4736 rows 0.79 ms) rather than jumps.
 std::uint64_t plan_chunks(unsigned L, std::uint64_t n, std::uint64_t c_max, int sms, int mode = MODE_U32,
                           bool gemm = false) {
     const double per_jump = 0.43e-6 * 148.0 / (double)sms;
@@ -648,11 +648,14 @@ std::uint64_t plan_chunks(unsigned L, std::uint64_t n, std::uint64_t c_max, int 
         return std::max(floor_s, jobs * per_jump);
     };
     const bool fused = mode == MODE_XOR;
-    const double r_lane = fused ? 5.5e8 : 3.2e8, peak_sm = (fused ? 3.4e12 : 1.6e12) / 148.0;
+    // store modes saturate at ~1.6e12 4-byte elements/s per GPU; doubles (one
+    // per word) at ~5.1e11/s (measured at L=8: 4.1 TB/s)
+    const bool dbl = mode == MODE_F64 || mode == MODE_F64_REAL3;
+    const double r_lane = fused ? 5.5e8 : 3.2e8, peak_sm = (fused ? 3.4e12 : dbl ? 5.1e11 : 1.6e12) / 148.0;
     auto t_pos = [&](std::uint64_t C) -> double {
         const double rows = double(C) * L;
         if (gemm && rows >= (double)gemm_min_rows())
-            return std::min(t_jump(double(C - 1) * L), 0.12e-3 + rows * 1.4e-7 * 148.0 / (double)sms);
+            return std::min(t_jump(double(C - 1) * L), 0.03e-3 + rows * 1.65e-7 * 148.0 / (double)sms);
         return t_jump(double(C - 1) * L);
     };
     auto t = [&](std::uint64_t C) {
@@ -717,13 +720,15 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
         std::max<std::uint64_t>(1, xor_groups ? std::min<std::uint64_t>(max_grid / groups, (std::uint64_t)sms)
                                               : max_grid / groups),
         nb);
-    // a fused-XOR fill of the same size as the previous one, with a
-    // positioning matrix for its block delta already built, is planned with
-    // the GEMM cost (validated for XOR: 7.4 -> 7.1 ms per 2^34 words at L=32;
-    // the store modes' rate model is calibrated for the jump-positioned shapes)
-    const bool gemm_plan = mode == MODE_XOR && h->positioning != 1 && h->last_fill_n == n && h->gemm &&
-                           h->gemm->last_valid && b0 > h->gemm->last_b0 &&
-                           usable_base(*h->gemm, b0 - h->gemm->last_b0) != 0;
+    // a fill of the same size as the previous one is planned with the GEMM
+    // positioning cost (its block delta's matrix is built once the delta
+    // repeats): fused XOR once that matrix exists (7.4 -> 7.1 ms per 2^34
+    // words at L=32), the other modes from the first repeat on (config 1,
+    // 2^26 words at L=16: 38 jump-positioned chunks 0.57 ms per fill -> 64
+    // GEMM-positioned chunks 0.35 ms)
+    const bool repeat = h->positioning != 1 && h->last_fill_n == n;
+    const bool gemm_plan = repeat && (mode != MODE_XOR || (h->gemm && h->gemm->last_valid && b0 > h->gemm->last_b0 &&
+                                                           usable_base(*h->gemm, b0 - h->gemm->last_b0) != 0));
     std::uint64_t C = h->max_chunks ? std::min<std::uint64_t>(c_max, h->max_chunks)
                                     : plan_chunks(h->L, n, c_max, sms, mode, gemm_plan);
     static const bool debug = std::getenv("VMT_DEBUG") != nullptr;
@@ -759,8 +764,17 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
             const std::uint64_t delta = b0 - gp.last_b0;
             if (gp.seen.size() > 64)
                 gp.seen.clear();
-            const int seen = ++gp.seen[delta];
-            // build the 400 MB matrix only for a delta that repeats
+            ++gp.seen[delta];
+            // build the 200 MB matrix only for a delta that repeats; deltas up
+            // to 4 blocks apart count as one (a fill size that is not a
+            // multiple of the block alternates between D and D+1, and one
+            // matrix for D serves both, capi_gemmpos.inl)
+            int seen = 0;
+            for (std::uint64_t k = 0; k <= 4 && k < delta; ++k) {
+                auto it = gp.seen.find(delta - k);
+                if (it != gp.seen.end())
+                    seen += it->second;
+            }
             if (usable_base(gp, delta) || seen >= 2 || h->positioning == 2) {
                 h->chunks_alt.reserve((size_t)C * kN * h->L);
                 try {
