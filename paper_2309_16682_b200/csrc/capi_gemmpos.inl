@@ -162,10 +162,17 @@ bool posmma_launch(GemmPos& gp, std::uint64_t delta, const std::uint32_t* src, s
     auto it = gp.tmaps.find(delta);
     if (gp.fp4 != 1 || it == gp.tmaps.end() || !gp.mats.count(delta))
         return false;
-    static bool attr = false;
-    if (!attr) {
-        VMT_CUDA(cudaFuncSetAttribute(vmt_posmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPmSmem));
-        attr = true;
+    {
+        // function attributes are per device (vmt_multi_gpu_fill drives several)
+        static std::mutex mu;
+        static std::set<int> done;
+        int dev = 0;
+        VMT_CUDA(cudaGetDevice(&dev));
+        std::lock_guard<std::mutex> lk(mu);
+        if (!done.count(dev)) {
+            VMT_CUDA(cudaFuncSetAttribute(vmt_posmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPmSmem));
+            done.insert(dev);
+        }
     }
     const std::uint64_t rows_pad = (rows + kPmM - 1) / kPmM * kPmM;
     gp.pm_a.reserve(rows_pad * kWB / 2);

@@ -204,3 +204,30 @@ def test_tensor_core_prefetch_matches_polynomial_jumps(L, n, gap):
     tc.fill_u32(b2)
     torch.cuda.synchronize()
     assert torch.equal(i32(a2), i32(b2))
+
+
+def test_tensor_core_prefetch_host_destination_and_streams():
+    """The prefetch in the host-destination path (1 GiB staged segments) and
+    with the caller switching CUDA streams between fills: identical words."""
+    n = (1 << 28) * 3 + 1234  # three full segments + a ragged one
+    ref = V.VmtGenerator(99, V.VmtConfig(32))
+    ref.set_positioning(1)
+    ref.set_prefetch(0)
+    tc = V.VmtGenerator(99, V.VmtConfig(32))
+    tc.set_prefetch(2)
+    a = torch.empty(n, dtype=torch.uint32, pin_memory=True)
+    b = torch.empty(n, dtype=torch.uint32, pin_memory=True)
+    ref.fill_u32(a)
+    tc.fill_u32(b)
+    assert torch.equal(i32(a), i32(b))
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    m = 1 << 27
+    da = torch.empty(m, dtype=torch.uint32, device="cuda")
+    db = torch.empty(m, dtype=torch.uint32, device="cuda")
+    for i in range(8):
+        s = streams[i % 2]
+        ref.fill_u32(da)
+        tc.fill_u32(db, stream=s.cuda_stream)
+        torch.cuda.synchronize()
+        assert torch.equal(i32(da), i32(db)), i
+    assert tc.prefetch_stats()["used"] >= 2, tc.prefetch_stats()
