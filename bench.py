@@ -287,7 +287,7 @@ def extras(dev) -> dict:
     jumped = torch.empty_like(states)
     s = timed(lambda: V.jump_states(states, dists, out=jumped), reps=2)
     out["c5_4096_jumps_64bit"] = {"value": 4096 / s, "unit": "state jumps/s", "ms": s * 1e3,
-                                  "note": "6 digit-table polynomial jumps per state (bits 16..63 of the 64-bit distance) + a direct advance by the low 16 bits"}
+                                  "note": "4 polynomial jumps per state from 12-bit digit tables (bits 16..63 of the 64-bit distance) + a direct advance by the low 16 bits"}
     # fused statistics consumer (monobit + chi2 byte histogram), 2^32 words, nothing stored
     n = 1 << 32
     g = V.VmtGenerator(5489, V.VmtConfig(32))

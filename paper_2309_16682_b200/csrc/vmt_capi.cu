@@ -242,9 +242,13 @@ void powers_parallel(const Poly& J, size_t count, std::vector<Poly>& out, size_t
 
 std::mutex g_poly_mu;
 
-// 8-bit digit tables T_j[v] = x^(v * 2^(8j)), j < 8, v < 256 (config 5 jumps).
+// 12-bit digit tables T_j[v] = x^(v * 2^(16 + 12 j)), j < 4, v < 4096, for
+// bits 16..63 of a 64-bit jump distance (config 5; the low 16 bits are
+// stepped directly): four jumps per state. 16384 polynomials (40 MB on the
+// device), built once per process by 16 host threads (~0.1 s).
+constexpr int kDigitBits = 12, kDigitBase = 16, kDigits = 4, kDigitVals = 1 << kDigitBits;
 struct DigitTables {
-    std::vector<Poly> host; // index j*256 + v (v=0 unused)
+    std::vector<Poly> host; // index j*4096 + v (v=0 unused)
     std::map<int, std::unique_ptr<DevBuf<std::uint64_t>>> dev;
 };
 DigitTables& digit_tables() {
@@ -252,18 +256,21 @@ DigitTables& digit_tables() {
     std::lock_guard<std::mutex> lk(g_poly_mu);
     if (t.host.empty()) {
         Gf2Field& F = Gf2Field::instance();
-        t.host.assign(8 * 256, Poly(kPolyWords, 0));
+        t.host.assign((size_t)kDigits * kDigitVals, Poly(kPolyWords, 0));
+        constexpr int kParts = 4; // threads per digit position
         std::vector<std::thread> th;
-        for (int j = 0; j < 8; ++j)
-            th.emplace_back([&, j] {
-                const Poly base = F.x_pow2(8 * j);
-                Poly cur = F.one();
-                t.host[j * 256] = cur;
-                for (int v = 1; v < 256; ++v) {
-                    cur = F.mulmod(cur, base);
-                    t.host[j * 256 + v] = cur;
-                }
-            });
+        for (int j = 0; j < kDigits; ++j)
+            for (int part = 0; part < kParts; ++part)
+                th.emplace_back([&, j, part] {
+                    const Poly base = F.x_pow2((unsigned)(kDigitBase + kDigitBits * j));
+                    const int v0 = part * (kDigitVals / kParts), v1 = v0 + kDigitVals / kParts;
+                    Poly cur = v0 == 0 ? F.one() : F.powmod(base, (std::uint64_t)v0);
+                    t.host[(size_t)j * kDigitVals + v0] = cur;
+                    for (int v = v0 + 1; v < v1; ++v) {
+                        cur = F.mulmod(cur, base);
+                        t.host[(size_t)j * kDigitVals + v] = cur;
+                    }
+                });
         for (auto& x : th)
             x.join();
     }
@@ -1422,18 +1429,18 @@ int vmt_jump_states(const uint32_t* src, uint64_t n, const uint64_t* distances, 
         DevBuf<long long> js, jd;
         DevBuf<int> jp;
         Counters cnt;
-        // digits 2..7 (bits 16..63) by table jumps, bits 0..15 by direct
+        // bits 16..63 by four 12-bit table jumps, bits 0..15 by direct
         // advance (vmt_advance_steps_kernel): F^d = F^(d_hi) F^(d_lo)
-        for (int j = 2; j < 8; ++j) {
+        for (int j = 0; j < kDigits; ++j) {
             std::vector<long long> vs, vd;
             std::vector<int> vp;
             for (std::uint64_t i = 0; i < n; ++i) {
-                const unsigned digit = (unsigned)((d[i] >> (8 * j)) & 0xFF);
+                const unsigned digit = (unsigned)((d[i] >> (kDigitBase + kDigitBits * j)) & (kDigitVals - 1));
                 if (!digit)
                     continue;
                 vs.push_back((long long)i * kN);
                 vd.push_back((long long)i * kN);
-                vp.push_back(j * 256 + (int)digit);
+                vp.push_back(j * kDigitVals + (int)digit);
             }
             // in place: each warp reads its whole state before writing it
             launch_jumps(st, buf.p, 1, buf.p, 1, tables, vs, vd, vp, js, jd, jp, cnt);
