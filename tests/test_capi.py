@@ -127,6 +127,9 @@ def test_argument_errors_without_gpu():
     assert lib.vmt_vec_mat_mul(None, 1, None, None, 0, None) == _capi.VMT_EINVAL
     assert lib.vmt_jump_states_matrix(None, 1, None, None, 0, None) == _capi.VMT_EINVAL
     assert lib.vmt_create(1, 3, 0, 0, ctypes.byref(h)) == _capi.VMT_EINVAL
+    u = ctypes.c_uint64()
+    assert lib.vmt_set_prefetch(None, _capi.VMT_PREFETCH_TENSOR) == _capi.VMT_EINVAL
+    assert lib.vmt_prefetch_stats(None, ctypes.byref(u), ctypes.byref(u)) == _capi.VMT_EINVAL
     with pytest.raises(V.InvalidArgument):
         V.write_jump_matrix_file("/tmp/never.vmtj", np.zeros(5, np.uint64), 1)
     assert b"invalid" in lib.vmt_status_string(_capi.VMT_EINVAL)
