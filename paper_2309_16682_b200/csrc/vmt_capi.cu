@@ -20,6 +20,7 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <tuple>
 #include <vector>
 
 #include "../../include/vmt19937_b200.h"
@@ -138,14 +139,14 @@ int prepare_gen(int dev, GenFn fn, int nt, int smem) {
     return d.occ[key];
 }
 
-// Whether one vmt_posmma_kernel CTA fits on an SM beside one CTA of the
+// Whether one vmt_posmma_kernel CTA fits on an SM beside per_sm CTAs of the
 // generation kernel `fn` (shared memory incl. the 1 KB per-CTA reservation,
 // registers, threads).
-bool posmma_fits(int dev, GenFn fn, int nt, int smem) {
+bool posmma_fits(int dev, GenFn fn, int nt, int smem, int per_sm) {
     static std::mutex mu;
-    static std::map<std::pair<int, const void*>, bool> memo;
+    static std::map<std::tuple<int, const void*, int>, bool> memo;
     std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_pair(dev, reinterpret_cast<const void*>(fn));
+    auto key = std::make_tuple(dev, reinterpret_cast<const void*>(fn), per_sm);
     auto it = memo.find(key);
     if (it != memo.end())
         return it->second;
@@ -159,9 +160,9 @@ bool posmma_fits(int dev, GenFn fn, int nt, int smem) {
     auto regs = [](int per_thread, int threads) { // allocation unit: 256 registers per warp
         return ((per_thread * 32 + 255) / 256 * 256) * ((threads + 31) / 32);
     };
-    const bool ok = smem + 1024 + kPmSmem + 1024 <= sm_smem &&
-                    regs(ga.numRegs, nt) + regs(pa.numRegs, kPmThreads) <= sm_regs &&
-                    nt + kPmThreads <= sm_threads && !std::getenv("VMT_NO_TC_PREFETCH");
+    const bool ok = per_sm * (smem + 1024) + kPmSmem + 1024 <= sm_smem &&
+                    per_sm * regs(ga.numRegs, nt) + regs(pa.numRegs, kPmThreads) <= sm_regs &&
+                    per_sm * nt + kPmThreads <= sm_threads && !std::getenv("VMT_NO_TC_PREFETCH");
     if (ok) {
         // both kernels ask for the full shared-memory carveout: an SM whose
         // generation CTA ran with the smallest carveout that fits it (132 KB)
@@ -830,10 +831,14 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     std::uint64_t next_b0 = 0;
     const std::uint64_t grid = C * groups;
     // the tensor-core form runs beside the generation kernel: only when that
-    // kernel leaves room for one vmt_posmma_kernel CTA on every SM it uses
+    // kernel runs one CTA per SM and leaves room for one vmt_posmma_kernel
+    // CTA (the 32-lane store kernel). The fused-XOR kernel (4 lane-group CTAs
+    // per SM) would also fit, but it is issue-bound rather than store-bound
+    // and loses more to the co-resident GEMM than the serial GEMM costs
+    // (measured 6.50 vs 6.40 ms per 2^34 words).
     const bool tc_pref = h->prefetch == VMT_PREFETCH_TENSOR && h->positioning != 1 && h->gemm &&
                          C * h->L >= gemm_min_rows() && grid <= (std::uint64_t)sms && occ == 1 &&
-                         posmma_fits(h->device, fn, v.NT, smem);
+                         posmma_fits(h->device, fn, v.NT, smem, 1);
     if ((h->prefetch == VMT_PREFETCH_JUMPS || tc_pref) && C > 1 && n >= kPrefetchMinWords) {
         const std::uint64_t gap = (h->last_end != ~0ull && P0 >= h->last_end) ? P0 - h->last_end : 0;
         const std::uint64_t P0n = P1 + gap;
