@@ -382,10 +382,12 @@ struct AffineJobs {
 // Launches the jump kernel with jobs given by an affine map of the job index
 // (no host tables, fully asynchronous).
 void launch_jumps_affine(cudaStream_t st, const std::uint32_t* src, int src_stride, std::uint32_t* dst,
-                         int dst_stride, const std::uint64_t* d_polys, const AffineJobs& a, Counters& cnt) {
+                         int dst_stride, const std::uint64_t* d_polys, const AffineJobs& a, Counters& cnt,
+                         const int* d_job_poly = nullptr) {
     if (a.n == 0)
         return;
     JumpParams jp{};
+    jp.job_poly = d_job_poly; // per-job polynomial index (else affine p_a, p_b, p_c)
     jp.src = src;
     jp.dst = dst;
     jp.polys = d_polys;
@@ -1431,24 +1433,26 @@ int vmt_jump_states(const uint32_t* src, uint64_t n, const uint64_t* distances, 
             VMT_CUDA(cudaMemcpy(d.data(), distances, n * 8, cudaMemcpyDeviceToHost));
         else
             std::memcpy(d.data(), distances, n * 8);
-        DevBuf<long long> js, jd;
-        DevBuf<int> jp;
-        Counters cnt;
         // bits 16..63 by four 12-bit table jumps, bits 0..15 by direct
-        // advance (vmt_advance_steps_kernel): F^d = F^(d_hi) F^(d_lo)
+        // advance (vmt_advance_steps_kernel): F^d = F^(d_hi) F^(d_lo). The
+        // per-job table indices of all four digits go up in one copy and the
+        // launches follow back to back (a zero digit jumps by T_j[0] = 1).
+        Counters cnt;
+        std::vector<int> pidx((size_t)kDigits * n);
+        for (int j = 0; j < kDigits; ++j)
+            for (std::uint64_t i = 0; i < n; ++i)
+                pidx[(size_t)j * n + i] =
+                    j * kDigitVals + (int)((d[i] >> (kDigitBase + kDigitBits * j)) & (kDigitVals - 1));
+        DevBuf<int> dp;
+        dp.reserve(pidx.size());
+        VMT_CUDA(cudaMemcpyAsync(dp.p, pidx.data(), pidx.size() * sizeof(int), cudaMemcpyHostToDevice, st));
         for (int j = 0; j < kDigits; ++j) {
-            std::vector<long long> vs, vd;
-            std::vector<int> vp;
-            for (std::uint64_t i = 0; i < n; ++i) {
-                const unsigned digit = (unsigned)((d[i] >> (kDigitBase + kDigitBits * j)) & (kDigitVals - 1));
-                if (!digit)
-                    continue;
-                vs.push_back((long long)i * kN);
-                vd.push_back((long long)i * kN);
-                vp.push_back(j * kDigitVals + (int)digit);
-            }
-            // in place: each warp reads its whole state before writing it
-            launch_jumps(st, buf.p, 1, buf.p, 1, tables, vs, vd, vp, js, jd, jp, cnt);
+            AffineJobs a;
+            a.n = (int)n;
+            a.div = 1;
+            a.s_a = kN; // job i: state i, in place (each warp reads its whole state before writing it)
+            a.d_a = kN;
+            launch_jumps_affine(st, buf.p, 1, buf.p, 1, tables, a, cnt, dp.p + (size_t)j * n);
         }
         DevBuf<unsigned long long> dd;
         dd.reserve(n);

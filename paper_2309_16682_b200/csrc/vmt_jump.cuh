@@ -201,7 +201,8 @@ __global__ void __launch_bounds__(32 * SPLIT, (SPLIT == 1 ? VMT_JUMP_MINB : 32 /
         const long long a = job / p.div, b = job % p.div;
         so = a * p.s_a + b * p.s_b + p.s_c;
         dof = a * p.d_a + b * p.d_b + p.d_c;
-        pidx = (int)(a * p.p_a + b * p.p_b + p.p_c);
+        // (a job_poly table may still supply the polynomial per job)
+        pidx = p.job_poly != nullptr ? p.job_poly[job] : (int)(a * p.p_a + b * p.p_b + p.p_c);
     }
     const std::uint32_t* src = p.src + so;
     for (int k = lane; k < kN; k += 32)
