@@ -464,28 +464,42 @@ def main():
     e2e = None
     out = None  # the 64 GiB device buffer is no longer needed
     torch.cuda.empty_cache()
+    # (N > 1: 2^32 words = 16 GiB of pinned host memory per rank instead of
+    # the full 64 GiB share, so 8 ranks pin 128 GiB rather than 512 GiB; the
+    # number is PCIe-bound and does not depend on the size past a few GiB)
+    ew = count if world == 1 else min(count, 1 << 32)
+    Te = ew * world
     if not args.no_e2e and args.mode == "store":
+        host, kind = None, None
         try:
-            host = torch.empty(count, dtype=torch.uint32, pin_memory=True)
+            host = torch.empty(ew, dtype=torch.uint32, pin_memory=True)
             kind = "pinned"
         except Exception:
-            host = np.empty(count, np.uint32)
-            kind = "pageable"
-        g.seek(start)
-        g.fill_u32(host)  # warm-up
-        g.skip(T - count)
+            if world == 1:
+                host = np.empty(ew, np.uint32)
+                kind = "pageable"
+        ok = torch.tensor([1 if host is not None else 0], device=coll)
         if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            g.fill_u32(host)
-            g.skip(T - count)
-        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
-        e2e_s = max_over_ranks(e2e_s, coll)
-        e2e = {"value": T / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": T * 4,
-               "ms_per_step": e2e_s * 1e3, "host_buffer": kind, "steps": args.e2e_steps}
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            e2e = {"unavailable": "no pinned host memory for the end-to-end buffer on some rank"}
+        else:
+            g.seek(rank * ew)
+            g.fill_u32(host)  # warm-up
+            g.skip(Te - ew)
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            for _ in range(args.e2e_steps):
+                g.fill_u32(host)
+                g.skip(Te - ew)
+            e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+            e2e_s = max_over_ranks(e2e_s, coll)
+            e2e = {"value": Te / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": Te * 4,
+                   "ms_per_step": e2e_s * 1e3, "host_buffer": kind, "steps": args.e2e_steps,
+                   "words_per_rank": ew}
         # the link the e2e number is bound by: a plain 1 GiB pinned D2H copy
-        if kind == "pinned":
+        if kind == "pinned" and "value" in e2e:
             src = torch.empty(1 << 28, dtype=torch.uint32, device=dev)
             best = 0.0
             for _ in range(3):
@@ -494,8 +508,8 @@ def main():
                 host[: 1 << 28].copy_(src, non_blocking=True)
                 torch.cuda.synchronize()
                 best = max(best, (1 << 30) / (time.perf_counter() - t1) / 1e9)
-            e2e["link_probe"] = {"d2h_memcpy_gbs": best, "e2e_gbs": T * 4 / e2e_s / 1e9 / world,
-                                 "frac": T * 4 / e2e_s / 1e9 / world / best,
+            e2e["link_probe"] = {"d2h_memcpy_gbs": best, "e2e_gbs": Te * 4 / e2e_s / 1e9 / world,
+                                 "frac": Te * 4 / e2e_s / 1e9 / world / best,
                                  "note": "pinned 1 GiB cudaMemcpy D2H (PCIe): the e2e fill moves 4 B per word "
                                          "over the same link"}
             del src

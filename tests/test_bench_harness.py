@@ -39,10 +39,12 @@ def test_bench_single_and_multi_rank_paths():
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] <= 1.2 and r["peak"] > 0
     assert one["gpu_launches"] >= 3 and one["e2e"]["d2h_bytes_per_step"] == 4 << 30
     shared = {"VMT_BENCH_SHARED_GPU": "1"}
-    weak = run(["--gpus", "2", "--words", words, "--steps", "3", "--warmup", "3", "--no-e2e"], shared, 2, 29562)
+    weak = run(["--gpus", "2", "--words", words, "--steps", "3", "--warmup", "3", "--no-extras"], shared, 2, 29562)
     strong = run(["--gpus", "2", "--words", str(1 << 30), "--scaling", "strong", "--steps", "3", "--warmup", "3",
                   "--no-e2e"], shared, 2, 29563)
     assert weak["n_gpus"] == strong["n_gpus"] == 2
+    # N > 1 end to end: every rank fills its own pinned host buffer
+    assert weak["e2e"]["d2h_bytes_per_step"] == 2 * 4 * (1 << 29) and weak["e2e"]["value"] > 0
     assert weak["checksum_xor"] == strong["checksum_xor"] == one["checksum_xor"]
 
 
