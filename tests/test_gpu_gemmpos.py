@@ -171,16 +171,16 @@ def test_gemm_positioned_stream_pinned_to_oracle(golden):
 
 @pytest.mark.parametrize("L,n,gap", [(32, (1 << 26) + 777, 0), (32, 1 << 27, 4321), (16, 1 << 27, 0),
                                      (32, 1 << 32, 0)])
-def test_tensor_core_prefetch_matches_polynomial_jumps(L, n, gap):
+def test_tensor_core_prefetch_matches_polynomial_jumps(L, n, gap, chunks=148):
     """VMT_PREFETCH_TENSOR: the next fill's chunk states come from the
     hand-written tcgen05 kernel (vmt_posmma.cuh) running beside the generation
     kernel; every fill must equal the jump-positioned reference."""
     ref = V.VmtGenerator(4242, V.VmtConfig(L))
-    ref.set_tuning(max_chunks=148)
+    ref.set_tuning(max_chunks=chunks)
     ref.set_positioning(1)
     ref.set_prefetch(0)
     tc = V.VmtGenerator(4242, V.VmtConfig(L))
-    tc.set_tuning(max_chunks=148)
+    tc.set_tuning(max_chunks=chunks)
     tc.set_prefetch(2)
     a = torch.empty(n, dtype=torch.uint32, device="cuda")
     b = torch.empty(n, dtype=torch.uint32, device="cuda")
@@ -231,3 +231,9 @@ def test_tensor_core_prefetch_host_destination_and_streams():
         torch.cuda.synchronize()
         assert torch.equal(i32(da), i32(db)), i
     assert tc.prefetch_stats()["used"] >= 2, tc.prefetch_stats()
+
+
+def test_tensor_core_prefetch_padded_rows():
+    """99 chunks x 32 lanes = 3168 lane states: the last 128-row tile of the
+    tcgen05 GEMM is padded with zero rows whose results are not stored."""
+    test_tensor_core_prefetch_matches_polynomial_jumps(32, (1 << 27) + 99, 0, chunks=99)
