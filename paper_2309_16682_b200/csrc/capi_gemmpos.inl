@@ -41,6 +41,7 @@ struct GemmPos {
     std::map<std::uint64_t, std::unique_ptr<DevBuf<std::int8_t>>> mats; // delta -> F^(624 delta), word-bit
     // TMA descriptors of the FP4 matrices (B operand of vmt_posmma_kernel)
     std::map<std::uint64_t, CUtensorMap> tmaps;
+    std::map<std::uint64_t, CUtensorMap> tmaps2; // 104-row boxes for the CTA-pair kernel
     DevBuf<std::int8_t> pm_a; // FP4 state operand of the co-resident prefetch
     CUtensorMap pm_tmap_a;
     const void* pm_tmap_ptr = nullptr;
@@ -159,8 +160,10 @@ bool make_tmap_fp4(CUtensorMap& m, const void* base, std::uint64_t rows, unsigne
 // for exactly this delta.
 bool posmma_launch(GemmPos& gp, std::uint64_t delta, const std::uint32_t* src, std::uint32_t* dst, unsigned L,
                    std::uint64_t rows, int sms, cudaStream_t st) {
-    auto it = gp.tmaps.find(delta);
-    if (gp.fp4 != 1 || it == gp.tmaps.end() || !gp.mats.count(delta))
+    // the CTA-pair kernel (cta_group::2) unless VMT_POSMMA_SINGLE is set
+    static const bool pair = std::getenv("VMT_POSMMA_SINGLE") == nullptr;
+    auto it = (pair ? gp.tmaps2 : gp.tmaps).find(delta);
+    if (gp.fp4 != 1 || it == (pair ? gp.tmaps2 : gp.tmaps).end() || !gp.mats.count(delta))
         return false;
     {
         // function attributes are per device (vmt_multi_gpu_fill drives several)
@@ -171,10 +174,13 @@ bool posmma_launch(GemmPos& gp, std::uint64_t delta, const std::uint32_t* src, s
         std::lock_guard<std::mutex> lk(mu);
         if (!done.count(dev)) {
             VMT_CUDA(cudaFuncSetAttribute(vmt_posmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPmSmem));
+            VMT_CUDA(
+                cudaFuncSetAttribute(vmt_posmma2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2Smem));
             done.insert(dev);
         }
     }
-    const std::uint64_t rows_pad = (rows + kPmM - 1) / kPmM * kPmM;
+    const std::uint64_t tile_rows = pair ? 2 * kPmM : kPmM;
+    const std::uint64_t rows_pad = (rows + tile_rows - 1) / tile_rows * tile_rows;
     gp.pm_a.reserve(rows_pad * kWB / 2);
     if (gp.pm_tmap_ptr != gp.pm_a.p || gp.pm_tmap_rows != rows_pad) {
         if (!make_tmap_fp4(gp.pm_tmap_a, gp.pm_a.p, rows_pad, kPmM))
@@ -193,9 +199,12 @@ bool posmma_launch(GemmPos& gp, std::uint64_t delta, const std::uint32_t* src, s
     pp.dst = dst;
     pp.L = (int)L;
     pp.rows = (int)rows;
-    pp.m_tiles = (int)(rows_pad / kPmM);
+    pp.m_tiles = (int)(rows_pad / tile_rows);
     const int tiles = pp.m_tiles * kPmNTiles;
-    vmt_posmma_kernel<<<std::min(tiles, sms), kPmThreads, kPmSmem, st>>>(gp.pm_tmap_a, it->second, pp);
+    if (pair)
+        vmt_posmma2_kernel<<<2 * std::min(tiles, sms / 2), kPmThreads, kP2Smem, st>>>(gp.pm_tmap_a, it->second, pp);
+    else
+        vmt_posmma_kernel<<<std::min(tiles, sms), kPmThreads, kPmSmem, st>>>(gp.pm_tmap_a, it->second, pp);
     VMT_CUDA(cudaGetLastError());
     return true;
 }
@@ -243,6 +252,7 @@ const std::int8_t* gemm_matrix(vmt_generator* h, GemmPos& gp, std::uint64_t delt
         VMT_CUDA(cudaStreamSynchronize(st));
         gp.mats.erase(victim);
         gp.tmaps.erase(victim);
+        gp.tmaps2.erase(victim);
         gp.last_use.erase(victim);
     }
     Gf2Field& F = Gf2Field::instance();
@@ -254,6 +264,8 @@ const std::int8_t* gemm_matrix(vmt_generator* h, GemmPos& gp, std::uint64_t delt
     CUtensorMap tm;
     if (gp.fp4 == 1 && make_tmap_fp4(tm, p, kWB, kPmNH))
         gp.tmaps[delta] = tm;
+    if (gp.fp4 == 1 && make_tmap_fp4(tm, p, kWB, kP2BQ))
+        gp.tmaps2[delta] = tm;
     gp.mats[delta] = std::move(m);
     gp.last_use[delta] = gp.tick;
     return p;
@@ -341,6 +353,7 @@ bool gemm_position_exact(vmt_generator* h, GemmPos& gp, const std::uint32_t* src
         gp.fp4 = 0;
         gp.mats.clear();
         gp.tmaps.clear();
+        gp.tmaps2.clear();
         gp.last_use.clear();
     }
     const std::int8_t* mat = gemm_matrix(h, gp, delta, st);

@@ -265,4 +265,215 @@ __global__ void __launch_bounds__(kPmThreads, 1)
     }
 }
 
+// ---- CTA-pair form (cta_group::2) -------------------------------------------
+// The same product with M = 256 lane states per MMA across a cluster of two
+// CTAs on one TPC: each CTA holds its own 128 rows of A and HALF of every B
+// tile (104 of the 208 rows per MMA), the leader CTA issues
+// tcgen05.mma.cta_group::2 and each CTA's TMEM receives its 128 rows of the
+// accumulators. Per SM the tensor core reads (1/208 + 1/256) instead of
+// (1/208 + 1/128) operand bytes per MAC from shared memory, and the B tiles
+// cross L2 -> SM half as often: less of what the co-resident GEMM takes from
+// the generation kernel (§4.6).
+constexpr int kP2BQ = kPmNH / 2;                    // 104 B rows per CTA per MMA
+constexpr int kP2BQBytes = kP2BQ * kPmKE / 2;       // 6656
+constexpr int kP2Stages = 4;
+constexpr int kP2StageBytes = kPmABytes + 2 * kP2BQBytes; // 21504
+constexpr int kP2Smem = kP2Stages * kP2StageBytes + 1024 + 128;
+// kind::mxf4, M = 256 (pair), N = 208
+constexpr unsigned kP2Idesc = (1u << 7) | (1u << 10) | ((unsigned)(kPmNH >> 3) << 17) | (1u << 23) |
+                              ((256u >> 4) << 24);
+
+__device__ __forceinline__ unsigned cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of `p` (a shared::cta variable) in CTA `rank`
+__device__ __forceinline__ unsigned map_to_rank(const void* p, unsigned rank) {
+    unsigned out;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(smem_u32(p)), "r"(rank));
+    return out;
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* sdst, const CUtensorMap* map, int x, int y,
+                                                 unsigned bar_cluster, unsigned long long policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(sdst)),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(x), "r"(y), "r"(bar_cluster), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(unsigned long long* bar) {
+    // arrives on the barrier at the same offset in both CTAs of the pair
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((unsigned short)3)
+        : "memory");
+}
+__device__ __forceinline__ void tc_mma_mxf4_pair(unsigned tmem_d, unsigned long long adesc,
+                                                 unsigned long long bdesc, unsigned idesc, unsigned tmem_sfa,
+                                                 unsigned tmem_sfb, unsigned accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%4], [%5], p;\n\t}" ::"r"(
+            tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(tmem_sfa), "r"(tmem_sfb), "r"(accumulate)
+        : "memory");
+}
+
+// p.m_tiles = ceil(rows / 256) pair tiles; tmap_b boxes are 104 rows
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPmThreads, 1)
+    vmt_posmma2_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                       const PosMmaParams p) {
+    extern __shared__ unsigned char pm_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(pm_raw) + 1023) &
+                                                           ~static_cast<std::uintptr_t>(1023));
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + kP2Stages * kP2StageBytes);
+    unsigned long long* empty = full + kP2Stages;
+    unsigned long long* accf = empty + kP2Stages; // MMA -> epilogues (both CTAs)
+    unsigned long long* accd = accf + 1;           // epilogues (both CTAs) -> leader's MMA thread
+    unsigned* tmem_slot = reinterpret_cast<unsigned*>(accd + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned rank = cluster_rank();
+    const bool leader = rank == 0;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kP2Stages; ++s) {
+            mbar_init(&full[s], 1);  // leader: its producer's expect_tx for both CTAs' bytes
+            mbar_init(&empty[s], 1); // MMA commit, multicast to both CTAs
+        }
+        mbar_init(accf, 1);
+        mbar_init(accd, 8); // 4 epilogue warps x 2 CTAs
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&tmap_a)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&tmap_b)) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const unsigned tmem = *tmem_slot;
+    if (warp >= 2) { // unit scale factors in this CTA's TMEM columns [448, 512)
+        const unsigned one4 = 0x7F7F7F7Fu;
+#pragma unroll
+        for (int c0 = kPmSfCol; c0 < 512; c0 += 16)
+            asm volatile(
+                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                    tmem + ((unsigned)((warp & 3) * 32) << 16) + (unsigned)c0),
+                "r"(one4)
+                : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int ntiles = p.m_tiles * kPmNTiles;
+    if (warp == 0) {
+        if (lane == 0) {
+            const unsigned long long pol = l2_policy_evict_last();
+            unsigned it = 0;
+            for (int tile = pair; tile < ntiles; tile += npairs) {
+                const int n = tile / p.m_tiles, m = tile % p.m_tiles;
+                for (int ks = 0; ks < kPmKSteps; ++ks, ++it) {
+                    const int s = it % kP2Stages;
+                    const unsigned u = it / kP2Stages;
+                    if (u > 0)
+                        mbar_wait_parity(&empty[s], (u - 1) & 1);
+                    unsigned char* a = smem + s * kP2StageBytes;
+                    unsigned char* b = a + kPmABytes;
+                    if (leader)
+                        mbar_arrive_expect_tx(&full[s], 2 * kP2StageBytes);
+                    const unsigned fb = map_to_rank(&full[s], 0);
+                    const int kx = ks * (kPmKE / 2);
+                    tma_load_2d_pair(a, &tmap_a, kx, m * 2 * kPmM + (int)rank * kPmM, fb, pol);
+                    tma_load_2d_pair(b, &tmap_b, kx, n * kPmN + (int)rank * kP2BQ, fb, pol);
+                    tma_load_2d_pair(b + kP2BQBytes, &tmap_b, kx, n * kPmN + kPmNH + (int)rank * kP2BQ, fb, pol);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {
+            unsigned it = 0, tcount = 0;
+            for (int tile = pair; tile < ntiles; tile += npairs, ++tcount) {
+                if (tcount > 0) { // both CTAs' epilogues have read the previous accumulators
+                    mbar_wait_parity(accd, (tcount - 1) & 1);
+                    tc_fence_after();
+                }
+                for (int ks = 0; ks < kPmKSteps; ++ks, ++it) {
+                    const int s = it % kP2Stages;
+                    mbar_wait_parity(&full[s], (it / kP2Stages) & 1);
+                    tc_fence_after();
+                    const unsigned a = smem_u32(smem + s * kP2StageBytes);
+                    const unsigned b = a + kPmABytes;
+#pragma unroll
+                    for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+                            tc_mma_mxf4_pair(tmem + kPmNH * h, sw64_desc(a + 32 * kk),
+                                             sw64_desc(b + h * kP2BQBytes + 32 * kk), kP2Idesc, tmem + kPmSfCol,
+                                             tmem + kPmSfCol + 32, (ks | kk) != 0);
+                    tc_commit_pair(&empty[s]);
+                }
+                tc_commit_pair(accf);
+            }
+        }
+    } else {
+        const int rq = (warp & 3) * 32;
+        const int r = (int)rank * kPmM + rq + lane; // row within the 256-row pair tile
+        const unsigned accd_leader = map_to_rank(accd, 0);
+        unsigned tcount = 0;
+        for (int tile = pair; tile < ntiles; tile += npairs, ++tcount) {
+            const int n = tile / p.m_tiles, m = tile % p.m_tiles;
+            const int row = m * 2 * kPmM + r;
+            const bool valid = row < p.rows;
+            const int c = valid ? row / p.L : 0, t = valid ? row % p.L : 0;
+            mbar_wait_parity(accf, tcount & 1);
+            tc_fence_after();
+            std::uint32_t* dst = p.dst + (long long)c * kN * p.L + t;
+#pragma unroll 1
+            for (int j = 0; j < kPmN / 32; ++j) {
+                std::uint32_t v[32];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                      "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+                      "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
+                      "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
+                      "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(tmem + ((unsigned)rq << 16) + 32u * j));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                std::uint32_t w = 0;
+#pragma unroll
+                for (int b = 0; b < 32; ++b)
+                    w |= ((std::uint32_t)__float2int_rn(__uint_as_float(v[b])) & 1u) << b;
+                const int k = n * (kPmN / 32) + j;
+                if (valid)
+                    dst[(long long)k * p.L] = k == 0 ? (w & kUpperMask) : w;
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(accd_leader)
+                             : "memory");
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+
 } // namespace vmt_b200
