@@ -6,7 +6,7 @@
   jump  : vmt_jump_kernel, the bench's positioning launch (147 x 32 = 4704 jobs)
   stats : vmt_gen_kernel MODE_STATS (fused monobit + byte histogram), 2^32 words
   xor   : vmt_gen_kernel MODE_XOR (fused checksum), 2^32 words
-  posmma: vmt_posmma_kernel, the co-resident tcgen05 FP4 positioning GEMM
+  posmma: vmt_posmma2_kernel, the co-resident tcgen05 FP4 positioning GEMM (CTA pairs)
           (4736 lane states x F^(624 D)); under ncu it runs serialised, i.e.
           alone on the GPU (6 fills of 2^32 words; it launches from fill 3 on)
 Each target runs its call three times; profile with --launch-skip/-c on the

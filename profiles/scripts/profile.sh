@@ -16,6 +16,6 @@ done
 ncu --set full --clock-control none --import-source on -k regex:vmt_jump_kernel --launch-skip 2 -c 1 \
     -o $OUT/prof_jump -f python profiles/scripts/prof_target.py jump > $OUT/ncu_jump.log 2>&1
 python profiles/scripts/prof_target.py posmma || exit 1
-ncu --set full --clock-control none --import-source on -k regex:vmt_posmma_kernel --launch-skip 1 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:vmt_posmma --launch-skip 1 -c 1 \
     -o $OUT/prof_posmma -f python profiles/scripts/prof_target.py posmma > $OUT/ncu_posmma.log 2>&1
 ls -la $OUT
