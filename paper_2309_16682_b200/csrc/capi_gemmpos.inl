@@ -328,6 +328,18 @@ bool gemm_position_exact(vmt_generator* h, GemmPos& gp, const std::uint32_t* src
         const std::int8_t* mat = gemm_matrix(h, gp, delta, st);
         if (!mat)
             return false;
+        // from 2048 lane states on, our tcgen05 CTA-pair kernel (operand
+        // expansion + GEMM + packing epilogue: 0.81 vs 0.85 ms for 4736
+        // states) instead of cuBLASLt's GEMM between our expand and pack
+        // kernels (378 MB fp32 product); below that cuBLASLt's tiles balance
+        // better (config 1, 1200 states: 0.366 vs 0.375 ms per fill)
+        static const bool lt_only = std::getenv("VMT_POSITION_CUBLASLT") != nullptr;
+        if (!lt_only && rows >= 2048 &&
+            posmma_launch(gp, delta, src, dst, h->L, rows, device_info(h->device).sms, st)) {
+            h->cnt.other += 2;
+            h->cnt.gemm_positionings += 1;
+            return true;
+        }
         const long long nwords = (long long)rows * kN;
         const unsigned grid = (unsigned)((nwords + 255) / 256);
         // the block-scale layout tiles rows by 128: pad the state operand with
