@@ -158,13 +158,31 @@ bool make_tmap_fp4(CUtensorMap& m, const void* base, std::uint64_t rows, unsigne
 // (vmt_posmma.cuh), launched on `st` (a side stream, after the generation
 // kernel): the FP4 state operand, then the GEMM. false: no FP4 matrix cached
 // for exactly this delta.
+// the CTA-pair kernel (cta_group::2) unless VMT_POSMMA_SINGLE is set
+bool posmma_pair() {
+    static const bool pair = std::getenv("VMT_POSMMA_SINGLE") == nullptr;
+    return pair;
+}
+
+bool posmma_run(GemmPos& gp, const CUtensorMap& tmap_b, const std::uint32_t* src, std::uint32_t* dst, unsigned L,
+                std::uint64_t rows, int sms, cudaStream_t st, unsigned nl, unsigned lane0);
+
 bool posmma_launch(GemmPos& gp, std::uint64_t delta, const std::uint32_t* src, std::uint32_t* dst, unsigned L,
                    std::uint64_t rows, int sms, cudaStream_t st) {
-    // the CTA-pair kernel (cta_group::2) unless VMT_POSMMA_SINGLE is set
-    static const bool pair = std::getenv("VMT_POSMMA_SINGLE") == nullptr;
+    const bool pair = posmma_pair();
     auto it = (pair ? gp.tmaps2 : gp.tmaps).find(delta);
     if (gp.fp4 != 1 || it == (pair ? gp.tmaps2 : gp.tmaps).end() || !gp.mats.count(delta))
         return false;
+    gp.last_use[delta] = gp.tick;
+    return posmma_run(gp, it->second, src, dst, L, rows, sms, st, L, 0);
+}
+
+// Lanes [lane0, lane0 + nl) of every state of dst (interleaved [.][624][L])
+// = lanes [0, nl) of src times the FP4 matrix behind tmap_b (nl = L, lane0 =
+// 0: every lane, chunk positioning).
+bool posmma_run(GemmPos& gp, const CUtensorMap& tmap_b, const std::uint32_t* src, std::uint32_t* dst, unsigned L,
+                std::uint64_t rows, int sms, cudaStream_t st, unsigned nl, unsigned lane0) {
+    const bool pair = posmma_pair();
     {
         // function attributes are per device (vmt_multi_gpu_fill drives several)
         static std::mutex mu;
@@ -188,23 +206,24 @@ bool posmma_launch(GemmPos& gp, std::uint64_t delta, const std::uint32_t* src, s
         gp.pm_tmap_ptr = gp.pm_a.p;
         gp.pm_tmap_rows = rows_pad;
     }
-    gp.last_use[delta] = gp.tick;
     if (rows_pad > rows)
         VMT_CUDA(cudaMemsetAsync(gp.pm_a.p + rows * kWB / 2, 0, (rows_pad - rows) * kWB / 2, st));
     const long long nwords = (long long)rows * kN;
     vmt_states_to_fp4_kernel<<<(unsigned)((nwords + 255) / 256), 256, 0, st>>>(
-        src, (int)L, 0, (int)L, nwords, reinterpret_cast<std::uint8_t*>(gp.pm_a.p));
+        src, (int)L, 0, (int)nl, nwords, reinterpret_cast<std::uint8_t*>(gp.pm_a.p));
     VMT_CUDA(cudaGetLastError());
     PosMmaParams pp;
     pp.dst = dst;
     pp.L = (int)L;
     pp.rows = (int)rows;
+    pp.nl = (int)nl;
+    pp.lane0 = (int)lane0;
     pp.m_tiles = (int)(rows_pad / tile_rows);
     const int tiles = pp.m_tiles * kPmNTiles;
     if (pair)
-        vmt_posmma2_kernel<<<2 * std::min(tiles, sms / 2), kPmThreads, kP2Smem, st>>>(gp.pm_tmap_a, it->second, pp);
+        vmt_posmma2_kernel<<<2 * std::min(tiles, sms / 2), kPmThreads, kP2Smem, st>>>(gp.pm_tmap_a, tmap_b, pp);
     else
-        vmt_posmma_kernel<<<std::min(tiles, sms), kPmThreads, kPmSmem, st>>>(gp.pm_tmap_a, it->second, pp);
+        vmt_posmma_kernel<<<std::min(tiles, sms), kPmThreads, kPmSmem, st>>>(gp.pm_tmap_a, tmap_b, pp);
     VMT_CUDA(cudaGetLastError());
     return true;
 }
@@ -403,6 +422,7 @@ struct DephaseGemm {
     std::mutex mu;
     GemmPos gp; // cuBLASLt handle, scales, workspace, operand buffers
     std::map<std::pair<unsigned, unsigned>, std::unique_ptr<DevBuf<std::int8_t>>> mats;
+    std::map<std::pair<unsigned, unsigned>, CUtensorMap> tmaps; // for vmt_posmma(2)_kernel
     bool fp4_ok = true;
 };
 
@@ -437,13 +457,26 @@ bool dephase_by_gemm(int device, cudaStream_t st, unsigned ngen, unsigned L, uns
             if (D.mats.size() >= 8) {
                 VMT_CUDA(cudaStreamSynchronize(st));
                 D.mats.clear();
+                D.tmaps.clear();
             }
             std::unique_ptr<DevBuf<std::int8_t>> m(new DevBuf<std::int8_t>());
             build_gemm_matrix(F.powmod(F.x_pow2(q), s), true, *m, st);
             cnt.other += 1;
+            CUtensorMap tm;
+            if (make_tmap_fp4(tm, m->p, kWB, posmma_pair() ? kP2BQ : kPmNH))
+                D.tmaps[key] = tm;
             it = D.mats.emplace(key, std::move(m)).first;
         }
         const std::uint64_t rows = (std::uint64_t)ngen * n, rows_pad = (rows + 127) / 128 * 128;
+        // our tcgen05 kernel: lanes [s, s+n) written straight from the
+        // accumulators (no fp32 product pass)
+        static const bool lt_only = std::getenv("VMT_POSITION_CUBLASLT") != nullptr;
+        auto tm = D.tmaps.find(key);
+        if (!lt_only && tm != D.tmaps.end() && rows >= 2048 &&
+            posmma_run(D.gp, tm->second, states, states, L, rows, device_info(device).sms, st, n, s)) {
+            cnt.other += 2;
+            continue;
+        }
         const long long nwords = (long long)rows * kN;
         const unsigned grid = (unsigned)((nwords + 255) / 256);
         D.gp.a.reserve(rows_pad * kWB / 2);

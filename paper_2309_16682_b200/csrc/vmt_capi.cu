@@ -798,6 +798,8 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
                     cudaGetLastError();
                     VMT_CUDA(cudaStreamSynchronize(st));
                     gp.mats.clear();
+                    gp.tmaps.clear();
+                    gp.tmaps2.clear();
                     h->positioning = 1;
                 }
             }
@@ -1549,6 +1551,7 @@ int vmt_release_caches(int device) {
         if (it != g_dephase.end()) {
             std::lock_guard<std::mutex> lk2(it->second->mu);
             it->second->mats.clear();
+            it->second->tmaps.clear();
         }
     });
 }

@@ -55,8 +55,9 @@ constexpr int kPmSfCol = 448;              // TMEM columns [448, 512): unit scal
 struct PosMmaParams {
     std::uint32_t* dst;       // [C][624][L] jumped by the matrix (the next fill's)
     int L;
-    int rows;                 // C * L
-    int m_tiles;              // ceil(rows / 128)
+    int rows;                 // C * nl
+    int m_tiles;              // ceil(rows / 128) (pair kernel: ceil(rows / 256))
+    int nl, lane0;            // row r -> state r / nl, lane lane0 + r % nl (all lanes: nl = L, lane0 = 0)
 };
 
 // ---- tcgen05 / TMA primitives -------------------------------------------------
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(kPmThreads, 1)
             const int n = tile / p.m_tiles, m = tile % p.m_tiles;
             const int row = m * kPmM + r;
             const bool valid = row < p.rows;
-            const int c = valid ? row / p.L : 0, t = valid ? row % p.L : 0;
+            const int c = valid ? row / p.nl : 0, t = valid ? p.lane0 + row % p.nl : 0;
             // 13 state words (416 columns) of this row
             mbar_wait_parity(accf, tcount & 1);
             tc_fence_after();
@@ -436,7 +437,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPmThreads, 1)
             const int n = tile / p.m_tiles, m = tile % p.m_tiles;
             const int row = m * 2 * kPmM + r;
             const bool valid = row < p.rows;
-            const int c = valid ? row / p.L : 0, t = valid ? row % p.L : 0;
+            const int c = valid ? row / p.nl : 0, t = valid ? p.lane0 + row % p.nl : 0;
             mbar_wait_parity(accf, tcount & 1);
             tc_fence_after();
             std::uint32_t* dst = p.dst + (long long)c * kN * p.L + t;
