@@ -4,14 +4,19 @@
 // B) advance every chunk start by the same block delta D: chunk c of the next
 // fill is chunk c of this one jumped by 624*D words -- one and the same GF(2)
 // matrix F^(624 D) for all C*L lane states. Instead of C*L polynomial jumps
-// (~0.39 us of GPU each), the new states are one integer GEMM
+// (~0.39 us of GPU each), the new states are one GEMM
 //   new[C*L][19968] = old[C*L][19968] x F^(624 D)[19968][19968]  (mod 2)
-// in word-bit coordinates (vmt_matrix.cuh), on the tensor cores via cuBLAS(Lt)
-// (a plain library GEMM): FP4 e2m1 x FP4 with unit NVFP4 block scales and
-// fp32 accumulation (exact: 0/1 inputs, sums <= 19937) where cuBLASLt offers
-// it, else int8 x int8 -> int32; then packed back into words. The 400 MB int8 matrix for a delta is built once (19937 basis jumps
-// + expansion) when the delta repeats; two deltas are cached (a fill size
-// that is not a multiple of the block alternates between two).
+// in word-bit coordinates (vmt_matrix.cuh) with FP4 e2m1 0/1 operands, unit
+// block scales and fp32 accumulation (exact: sums <= 19937):
+//   * our tcgen05 kernels (vmt_posmma.cuh): the CTA-pair kernel, from 2048
+//     lane states on -- serially between fills, or co-resident with the
+//     generation kernel as the prefetch of the next fill (VMT_PREFETCH_TENSOR);
+//   * cuBLASLt's block-scaled FP4 GEMM between our operand and packing
+//     kernels (small row counts, and the fallback), else int8 x int8 -> int32
+//     where the library has no FP4 kernel.
+// The 200 MB FP4 matrix for a delta is built once (19937 basis jumps +
+// expansion) when the delta repeats; two are cached, and deltas up to 4 blocks
+// above a cached one reuse it (the rest regenerated in place).
 #include <cublasLt.h>
 #include <cublas_v2.h>
 #include <cudaTypedefs.h>
