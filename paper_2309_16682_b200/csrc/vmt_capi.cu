@@ -835,14 +835,16 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     std::uint64_t next_b0 = 0;
     const std::uint64_t grid = C * groups;
     // the tensor-core form runs beside the generation kernel: only when that
-    // kernel runs one CTA per SM and leaves room for one vmt_posmma_kernel
-    // CTA (the 32-lane store kernel). The fused-XOR kernel (4 lane-group CTAs
-    // per SM) would also fit, but it is issue-bound rather than store-bound
-    // and loses more to the co-resident GEMM than the serial GEMM costs
-    // (measured 6.50 vs 6.40 ms per 2^34 words).
+    // kernel's CTAs spread evenly over the SMs (one wave) and leave room for
+    // one positioning CTA on each. Not for the fused XOR: that kernel is
+    // issue-bound rather than store-bound and loses more to the co-resident
+    // GEMM than the serial GEMM costs (measured 6.53 vs 6.37 ms per 2^34
+    // words).
+    const int per_sm = (int)((grid + sms - 1) / (std::uint64_t)sms);
     const bool tc_pref = h->prefetch == VMT_PREFETCH_TENSOR && h->positioning != 1 && h->gemm &&
-                         C * h->L >= gemm_min_rows() && grid <= (std::uint64_t)sms && occ == 1 &&
-                         posmma_fits(h->device, fn, v.NT, smem, 1);
+                         mode != MODE_XOR && C * h->L >= gemm_min_rows() &&
+                         (grid <= (std::uint64_t)sms || grid % sms == 0) && per_sm <= occ &&
+                         posmma_fits(h->device, fn, v.NT, smem, per_sm);
     if ((h->prefetch == VMT_PREFETCH_JUMPS || tc_pref) && C > 1 && n >= kPrefetchMinWords) {
         const std::uint64_t gap = (h->last_end != ~0ull && P0 >= h->last_end) ? P0 - h->last_end : 0;
         const std::uint64_t P0n = P1 + gap;
