@@ -237,3 +237,23 @@ def test_tensor_core_prefetch_padded_rows():
     """99 chunks x 32 lanes = 3168 lane states: the last 128-row tile of the
     tcgen05 GEMM is padded with zero rows whose results are not stored."""
     test_tensor_core_prefetch_matches_polynomial_jumps(32, (1 << 27) + 99, 0, chunks=99)
+
+
+def test_tensor_core_prefetch_two_ctas_per_sm_f32():
+    """Config 2's shape: L=8, 2^28 float32 per fill, 296 chunks = two
+    generation CTAs per SM plus the co-resident positioning CTA."""
+    n = 1 << 28
+    ref = V.VmtGenerator(42, V.VmtConfig(8))
+    ref.set_positioning(1)
+    ref.set_prefetch(0)
+    tc = V.VmtGenerator(42, V.VmtConfig(8))
+    tc.set_prefetch(2)
+    a = torch.empty(n, dtype=torch.float32, device="cuda")
+    b = torch.empty(n, dtype=torch.float32, device="cuda")
+    for i in range(8):
+        ref.fill_f32(a)
+        tc.fill_f32(b)
+        torch.cuda.synchronize()
+        assert torch.equal(a.view(torch.int32), b.view(torch.int32)), i
+    st = tc.prefetch_stats()
+    assert st["tensor_prefetches"] >= 3 and st["used"] >= 3, st
