@@ -160,7 +160,8 @@ bool posmma_fits(int dev, GenFn fn, int nt, int smem, int per_sm) {
     auto regs = [](int per_thread, int threads) { // allocation unit: 256 registers per warp
         return ((per_thread * 32 + 255) / 256 * 256) * ((threads + 31) / 32);
     };
-    const bool ok = per_sm * (smem + 1024) + kPmSmem + 1024 <= sm_smem &&
+    const int pm_smem = std::getenv("VMT_POSMMA_SINGLE") ? kPmSmem : kP2Smem; // the kernel posmma_run launches
+    const bool ok = per_sm * (smem + 1024) + pm_smem + 1024 <= sm_smem &&
                     per_sm * regs(ga.numRegs, nt) + regs(pa.numRegs, kPmThreads) <= sm_regs &&
                     per_sm * nt + kPmThreads <= sm_threads && !std::getenv("VMT_NO_TC_PREFETCH");
     if (ok) {

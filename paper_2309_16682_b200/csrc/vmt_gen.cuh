@@ -91,12 +91,10 @@ struct GenShape {
         return (TMA && staged_mode<MODE>()) ? W * L * elem_bytes<MODE>() : 0;
     }
     // MODE_STATS: one byte-value histogram per lane position, hist[bin][lane]
-    // with a row stride of 64 counters (64 KB, columns 32..63 unused): a
-    // warp's 32 atomics always hit 32 different banks, and a counter's byte
-    // offset bin*256 + lane*4 is ONE byte permute of the word and lane*4
+    // (32 KB): a warp's 32 atomics always hit 32 different banks
     template <int MODE>
     __host__ __device__ static constexpr int hist_bytes() {
-        return MODE == MODE_STATS ? 256 * 64 * 4 : 0;
+        return MODE == MODE_STATS ? 256 * 32 * 4 : 0;
     }
     template <int MODE>
     __host__ __device__ static constexpr int smem() {
@@ -209,8 +207,7 @@ struct StageCtl {
     unsigned phase;   // mbarrier completions consumed so far
     bool prev_staged; // a bulk copy of buf is outstanding (not yet confirmed read)
     bool pending;     // tid 0's view of the same
-    std::uint32_t* hist; // MODE_STATS: the histogram base (hist[bin][64])
-    unsigned lane4;      // MODE_STATS: (tid & 31) * 4, this thread's column offset
+    std::uint32_t* hist; // MODE_STATS: this thread's histogram column (stride 32)
 };
 
 // One window of one thread: R new words of V lanes. base: slot of x_p for
@@ -283,13 +280,11 @@ __device__ __forceinline__ void gen_window(std::uint32_t* ring, int base, int a,
                 if (FULL || (g >= p.pos_begin && g < p.pos_end)) {
                     const std::uint32_t t = temper(nw[v]);
                     acc[0] += __popc(t);
-                    // one PRMT per byte forms the counter's byte offset
-                    // [lane*4, byte, 0, 0] = byte*256 + lane*4
-                    unsigned char* hb = reinterpret_cast<unsigned char*>(sc.hist);
-                    atomicAdd(reinterpret_cast<std::uint32_t*>(hb + __byte_perm(t, sc.lane4, 0x5504u)), 1u);
-                    atomicAdd(reinterpret_cast<std::uint32_t*>(hb + __byte_perm(t, sc.lane4, 0x5514u)), 1u);
-                    atomicAdd(reinterpret_cast<std::uint32_t*>(hb + __byte_perm(t, sc.lane4, 0x5524u)), 1u);
-                    atomicAdd(reinterpret_cast<std::uint32_t*>(hb + __byte_perm(t, sc.lane4, 0x5534u)), 1u);
+                    // PRMT extracts a byte zero-extended, one LEA forms the address
+                    atomicAdd(sc.hist + (__byte_perm(t, 0u, 0x4440u) << 5), 1u);
+                    atomicAdd(sc.hist + (__byte_perm(t, 0u, 0x4441u) << 5), 1u);
+                    atomicAdd(sc.hist + (__byte_perm(t, 0u, 0x4442u) << 5), 1u);
+                    atomicAdd(sc.hist + (__byte_perm(t, 0u, 0x4443u) << 5), 1u);
                 }
             }
         } else if (MODE == MODE_BENCH_TEMPER_XOR) {
@@ -396,8 +391,8 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::NT, GenShape<L, R,
     sc.phase = 0;
     sc.prev_staged = false;
     sc.pending = false;
-    sc.hist = reinterpret_cast<std::uint32_t*>(reinterpret_cast<unsigned char*>(ring) + S::RING_BYTES);
-    sc.lane4 = (unsigned)(tid & 31) * 4u;
+    sc.hist = reinterpret_cast<std::uint32_t*>(reinterpret_cast<unsigned char*>(ring) + S::RING_BYTES) +
+              (MODE == MODE_STATS ? (tid & 31) : 0);
     // bulk copies need the window's destination 16-byte aligned
     const bool tma_ok =
         kStaged &&
@@ -535,7 +530,7 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::NT, GenShape<L, R,
         for (int b = tid; b < 256; b += S::NT) {
             unsigned long long c = 0;
             for (int l = 0; l < 32; ++l)
-                c += h0[b * 64 + ((l + b) & 31)]; // rotated: the 32 threads of a warp read 32 banks
+                c += h0[b * 32 + ((l + b) & 31)]; // rotated: the 32 threads of a warp read 32 banks
             dst[1 + b] = c;
         }
         __syncthreads();
