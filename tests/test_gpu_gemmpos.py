@@ -257,3 +257,30 @@ def test_tensor_core_prefetch_two_ctas_per_sm_f32():
         assert torch.equal(a.view(torch.int32), b.view(torch.int32)), i
     st = tc.prefetch_stats()
     assert st["tensor_prefetches"] >= 3 and st["used"] >= 3, st
+
+
+def test_tensor_core_prefetch_two_generators_interleaved():
+    """Two handles with prefetches in flight at the same time (each on its own
+    side stream), fills interleaved, one destroyed mid-way: every word equals
+    its jump-positioned reference."""
+    n = (1 << 27) + 4321
+    refs = [V.VmtGenerator(s, V.VmtConfig(32)) for s in (11, 12)]
+    tcs = [V.VmtGenerator(s, V.VmtConfig(32)) for s in (11, 12)]
+    for r in refs:
+        r.set_tuning(max_chunks=148)
+        r.set_positioning(1)
+        r.set_prefetch(0)
+    for t in tcs:
+        t.set_tuning(max_chunks=148)
+        t.set_prefetch(2)
+    a = torch.empty(n, dtype=torch.uint32, device="cuda")
+    b = torch.empty(n, dtype=torch.uint32, device="cuda")
+    for i in range(7):
+        for k in range(len(tcs)):
+            refs[k].fill_u32(a)
+            tcs[k].fill_u32(b)
+            torch.cuda.synchronize()
+            assert torch.equal(i32(a), i32(b)), (i, k)
+        if i == 4:
+            del tcs[1], refs[1]  # destroyed with its prefetch possibly in flight
+    assert tcs[0].prefetch_stats()["used"] >= 3
