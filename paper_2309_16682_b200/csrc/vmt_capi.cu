@@ -342,38 +342,6 @@ void launch_jump_kernel(const JumpParams& jp, cudaStream_t st) {
     VMT_CUDA(cudaGetLastError());
 }
 
-// Launches the jump kernel on jobs (all host vectors; uploaded to dev scratch).
-void launch_jumps(cudaStream_t st, const std::uint32_t* src, int src_stride, std::uint32_t* dst, int dst_stride,
-                  const std::uint64_t* d_polys, const std::vector<long long>& jsrc,
-                  const std::vector<long long>& jdst, const std::vector<int>& jpoly, DevBuf<long long>& dsrc,
-                  DevBuf<long long>& ddst, DevBuf<int>& dpoly, Counters& cnt) {
-    const int n = (int)jsrc.size();
-    if (n == 0)
-        return;
-    dsrc.reserve(n);
-    ddst.reserve(n);
-    dpoly.reserve(n);
-    VMT_CUDA(cudaMemcpyAsync(dsrc.p, jsrc.data(), n * sizeof(long long), cudaMemcpyHostToDevice, st));
-    VMT_CUDA(cudaMemcpyAsync(ddst.p, jdst.data(), n * sizeof(long long), cudaMemcpyHostToDevice, st));
-    VMT_CUDA(cudaMemcpyAsync(dpoly.p, jpoly.data(), n * sizeof(int), cudaMemcpyHostToDevice, st));
-    JumpParams jp{};
-    jp.src = src;
-    jp.dst = dst;
-    jp.polys = d_polys;
-    jp.job_src = dsrc.p;
-    jp.job_dst = ddst.p;
-    jp.job_poly = dpoly.p;
-    jp.src_stride = src_stride;
-    jp.dst_stride = dst_stride;
-    jp.njobs = n;
-    launch_jump_kernel(jp, st);
-    cnt.jump += 1;
-    cnt.lane_jumps += n;
-    // the job tables are host vectors owned by the caller; make the upload
-    // complete before they can be released
-    VMT_CUDA(cudaStreamSynchronize(st));
-}
-
 struct AffineJobs {
     int n = 0, div = 1;
     long long s_a = 0, s_b = 0, s_c = 0, d_a = 0, d_b = 0, d_c = 0;
@@ -457,8 +425,6 @@ struct vmt_generator {
     DevBuf<unsigned long long> stat_partials; // per-CTA MODE_STATS partials [grid][257]
     DevBuf<std::uint32_t> scratch;   // device staging for host destinations
     DevBuf<std::uint64_t> tmp_poly;
-    DevBuf<long long> jsrc, jdst;
-    DevBuf<int> jpoly;
     std::uint32_t* hstage = nullptr; // pinned staging for single / block16 queries
     std::uint64_t hstage_cap = 0, hstage_start = 0;
     std::uint32_t* hsmall = nullptr; // pinned 4-byte readback
