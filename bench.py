@@ -508,10 +508,20 @@ def main():
                 host[: 1 << 28].copy_(src, non_blocking=True)
                 torch.cuda.synchronize()
                 best = max(best, (1 << 30) / (time.perf_counter() - t1) / 1e9)
-            e2e["link_probe"] = {"d2h_memcpy_gbs": best, "e2e_gbs": Te * 4 / e2e_s / 1e9 / world,
-                                 "frac": Te * 4 / e2e_s / 1e9 / world / best,
-                                 "note": "pinned 1 GiB cudaMemcpy D2H (PCIe): the e2e fill moves 4 B per word "
-                                         "over the same link"}
+            # sustained: 16 back-to-back 1 GiB copies into distinct parts of the buffer
+            parts = min(16, ew >> 28)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            for k in range(parts):
+                host[k << 28: (k + 1) << 28].copy_(src, non_blocking=True)
+            torch.cuda.synchronize()
+            sustained = parts * (1 << 30) / (time.perf_counter() - t1) / 1e9 if parts else None
+            e2e_gbs = Te * 4 / e2e_s / 1e9 / world
+            e2e["link_probe"] = {"d2h_memcpy_gbs": best, "d2h_memcpy_sustained_gbs": sustained,
+                                 "e2e_gbs": e2e_gbs, "frac": e2e_gbs / best,
+                                 "frac_of_sustained": e2e_gbs / sustained if sustained else None,
+                                 "note": "pinned cudaMemcpy D2H (PCIe), one 1 GiB copy (best of 3) and 16 "
+                                         "back to back: the e2e fill moves 4 B per word over the same link"}
             del src
         del host
 
