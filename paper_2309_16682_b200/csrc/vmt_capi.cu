@@ -1031,12 +1031,28 @@ void refill_stage(vmt_generator* h) {
 
 // Builds interleaved [624][L] de-phased states for `ngen` generators with
 // seeds seed0.. into dst (generator stride 624*L words).
+// Device buffers kept per host thread and device, reused across calls (no
+// cudaMalloc/cudaFree -- a device-wide sync -- per call). Slots: 0 seeds,
+// 1 batch states, 2 batch host staging, 3 jumped states (vmt_jump_states),
+// 4 its table indices, 5 its distances.
+template <class T>
+DevBuf<T>& thread_scratch(int device, int slot) {
+    thread_local std::map<std::pair<int, int>, std::unique_ptr<DevBuf<T>>> bufs;
+    auto& b = bufs[std::make_pair(device, slot)];
+    if (!b)
+        b.reset(new DevBuf<T>());
+    return *b;
+}
+DevBuf<std::uint32_t>& thread_scratch_u32(int device, int slot) { return thread_scratch<std::uint32_t>(device, slot); }
+
 void build_dephased(int device, cudaStream_t st, std::uint32_t seed0, unsigned ngen, unsigned L, unsigned q,
                     std::uint32_t* dst, DevBuf<std::uint64_t>& polybuf, Counters& cnt) {
     std::vector<std::uint32_t> seeds(ngen);
     for (unsigned g = 0; g < ngen; ++g)
         seeds[g] = seed0 + g;
-    DevBuf<std::uint32_t> dseeds;
+    // per-thread, per-device scratch: no cudaMalloc/cudaFree (a device-wide
+    // sync) per call
+    DevBuf<std::uint32_t>& dseeds = thread_scratch_u32(device, 0);
     dseeds.reserve(ngen);
     VMT_CUDA(cudaMemcpyAsync(dseeds.p, seeds.data(), ngen * 4, cudaMemcpyHostToDevice, st));
     vmt_seed_kernel<<<(ngen + 127) / 128, 128, 0, st>>>(dseeds.p, (int)ngen, dst, (long long)kN * L, (int)L);
@@ -1346,7 +1362,7 @@ int vmt_batch_fill_u32(uint32_t seed0, unsigned ngen, unsigned lanes, unsigned j
         DeviceGuard g(device);
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamPerThread;
         const unsigned q = jump_exponent == VMT_FULL_PERIOD ? vmt_full_period_exponent(lanes) : jump_exponent;
-        DevBuf<std::uint32_t> states;
+        DevBuf<std::uint32_t>& states = thread_scratch_u32(device, 1);
         DevBuf<std::uint64_t> polys;
         Counters cnt;
         states.reserve((size_t)ngen * kN * lanes);
@@ -1355,7 +1371,7 @@ int vmt_batch_fill_u32(uint32_t seed0, unsigned ngen, unsigned lanes, unsigned j
             return;
         const Variant& v = pick_variant(lanes, 0);
         const bool dev = is_device_ptr(dst);
-        DevBuf<std::uint32_t> scratch;
+        DevBuf<std::uint32_t>& scratch = thread_scratch_u32(device, 2);
         std::uint32_t* out = dst;
         if (!dev) {
             scratch.reserve((size_t)ngen * n_per_gen);
@@ -1393,7 +1409,7 @@ int vmt_jump_states(const uint32_t* src, uint64_t n, const uint64_t* distances, 
         DeviceGuard g(device);
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamPerThread;
         const std::uint64_t* tables = digit_tables_device(device);
-        DevBuf<std::uint32_t> buf;
+        DevBuf<std::uint32_t>& buf = thread_scratch_u32(device, 3);
         buf.reserve(n * kN);
         if (is_device_ptr(src))
             VMT_CUDA(cudaMemcpyAsync(buf.p, src, n * kN * 4, cudaMemcpyDeviceToDevice, st));
@@ -1414,7 +1430,7 @@ int vmt_jump_states(const uint32_t* src, uint64_t n, const uint64_t* distances, 
             for (std::uint64_t i = 0; i < n; ++i)
                 pidx[(size_t)j * n + i] =
                     j * kDigitVals + (int)((d[i] >> (kDigitBase + kDigitBits * j)) & (kDigitVals - 1));
-        DevBuf<int> dp;
+        DevBuf<int>& dp = thread_scratch<int>(device, 4);
         dp.reserve(pidx.size());
         VMT_CUDA(cudaMemcpyAsync(dp.p, pidx.data(), pidx.size() * sizeof(int), cudaMemcpyHostToDevice, st));
         for (int j = 0; j < kDigits; ++j) {
@@ -1425,7 +1441,7 @@ int vmt_jump_states(const uint32_t* src, uint64_t n, const uint64_t* distances, 
             a.d_a = kN;
             launch_jumps_affine(st, buf.p, 1, buf.p, 1, tables, a, cnt, dp.p + (size_t)j * n);
         }
-        DevBuf<unsigned long long> dd;
+        DevBuf<unsigned long long>& dd = thread_scratch<unsigned long long>(device, 5);
         dd.reserve(n);
         VMT_CUDA(cudaMemcpyAsync(dd.p, d.data(), n * 8, cudaMemcpyHostToDevice, st));
         vmt_advance_steps_kernel<<<(unsigned)((n + kStepWarps - 1) / kStepWarps), 32 * kStepWarps, 0, st>>>(
