@@ -78,11 +78,10 @@ void stat_counts(vmt_generator* h, std::uint64_t n, std::uint64_t* c, cudaStream
         n -= take;
     }
     if (n) {
-        DevBuf<unsigned long long> dout;
-        dout.reserve(kStatWords);
-        gpu_generate(h, MODE_STATS, nullptr, n, st, dout.p);
+        h->stat_out.reserve(kStatWords);
+        gpu_generate(h, MODE_STATS, nullptr, n, st, h->stat_out.p);
         std::vector<unsigned long long> g(kStatWords);
-        VMT_CUDA(cudaMemcpyAsync(g.data(), dout.p, kStatWords * 8, cudaMemcpyDeviceToHost, st));
+        VMT_CUDA(cudaMemcpyAsync(g.data(), h->stat_out.p, kStatWords * 8, cudaMemcpyDeviceToHost, st));
         VMT_CUDA(cudaStreamSynchronize(st));
         for (int j = 0; j < kStatWords; ++j)
             c[j] += g[j];

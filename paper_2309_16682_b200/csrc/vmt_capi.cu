@@ -423,6 +423,7 @@ struct vmt_generator {
     cudaEvent_t ev_chunks = nullptr, ev_pref = nullptr;
     DevBuf<std::uint32_t> partials;  // per-CTA xor partials
     DevBuf<unsigned long long> stat_partials; // per-CTA MODE_STATS partials [grid][257]
+    DevBuf<unsigned long long> stat_out;      // reduced MODE_STATS counts [257]
     DevBuf<std::uint32_t> scratch;   // device staging for host destinations
     DevBuf<std::uint64_t> tmp_poly;
     std::uint32_t* hstage = nullptr; // pinned staging for single / block16 queries
