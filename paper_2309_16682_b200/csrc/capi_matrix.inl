@@ -38,8 +38,10 @@ void vec_mat(const std::uint64_t* vecs, std::uint64_t n, const std::uint64_t* ma
 // effective state of the basis state e_i jumped by d steps (19937 jobs of
 // vmt_jump_kernel, in place on the basis states).
 void matrix_from_poly(const Poly& p, std::uint64_t* rows_dev, cudaStream_t st, Counters& cnt) {
-    DevBuf<std::uint32_t> states;
-    DevBuf<std::uint64_t> dp;
+    int dev = 0;
+    VMT_CUDA(cudaGetDevice(&dev));
+    DevBuf<std::uint32_t>& states = thread_scratch<std::uint32_t>(dev, 6); // 50 MB, reused
+    DevBuf<std::uint64_t>& dp = thread_scratch<std::uint64_t>(dev, 7);
     states.reserve((std::size_t)kDim * kN);
     dp.reserve(kPolyWords);
     VMT_CUDA(cudaMemcpyAsync(dp.p, p.data(), kPolyWords * 8, cudaMemcpyHostToDevice, st));
@@ -54,7 +56,7 @@ void matrix_from_poly(const Poly& p, std::uint64_t* rows_dev, cudaStream_t st, C
     launch_jumps_affine(st, states.p, 1, states.p, 1, dp.p, a, cnt);
     words_to_eff(states.p, kN, 1, reinterpret_cast<std::uint32_t*>(rows_dev), kDim, st);
     cnt.other += 2;
-    VMT_CUDA(cudaStreamSynchronize(st)); // states / dp are released on return
+    VMT_CUDA(cudaStreamSynchronize(st)); // the scratch is reused by the next call on this thread
 }
 
 // rows_out may be host or device memory.

@@ -1035,7 +1035,8 @@ void refill_stage(vmt_generator* h) {
 // Device buffers kept per host thread and device, reused across calls (no
 // cudaMalloc/cudaFree -- a device-wide sync -- per call). Slots: 0 seeds,
 // 1 batch states, 2 batch host staging, 3 jumped states (vmt_jump_states),
-// 4 its table indices, 5 its distances.
+// 4 its table indices, 5 its distances, 6/7 basis states and polynomial of a
+// jump-matrix build (capi_matrix.inl).
 template <class T>
 DevBuf<T>& thread_scratch(int device, int slot) {
     thread_local std::map<std::pair<int, int>, std::unique_ptr<DevBuf<T>>> bufs;
