@@ -269,9 +269,10 @@ class VmtGenerator:
     def set_tuning(self, max_chunks: int = 0, variant: int = 0) -> None:
         check(lib.vmt_set_tuning(self._h, max_chunks, variant))
 
-    def set_prefetch(self, mode: int = 1) -> None:
-        """0 off, 1 (or True) polynomial jumps on a side stream, 2 tcgen05 GEMM
-        beside the generation kernel (the default)."""
+    def set_prefetch(self, mode: int = _capi.VMT_PREFETCH_TENSOR) -> None:
+        """Positioning prefetch of the predicted next fill: 0 off, 1 (or True)
+        polynomial jumps on a side stream, 2 the tcgen05 GEMM beside the
+        generation kernel (what a new generator starts with)."""
         check(lib.vmt_set_prefetch(self._h, int(mode)))
 
     def prefetch_stats(self) -> dict:
