@@ -11,7 +11,7 @@ Sources:
   polynomials x^(2^q) mod P, q = 19932..19936, by plain repeated squaring
   (with the period check x^(2^19937) == x).
 
-Usage: python tests/golden/make_golden.py [--skip-ladder] [--only vmtj|stats|c4_full]
+Usage: python tests/golden/make_golden.py [--skip-ladder] [--only vmtj|stats|c4_full|c3_full]
 (--only SECTION recomputes one section into the existing golden.json)
 """
 from __future__ import annotations
@@ -112,6 +112,35 @@ def c4_full_section(r: RefLib, out: dict) -> None:
     print(f"c4 full checksum 0x{x:08x} {time.time() - t0:.1f}s", flush=True)
 
 
+C3_SEEDS = 1024
+C3_WORDS = 1 << 20
+
+
+def c3_full_section(r: RefLib, out: dict) -> None:
+    """Config 3 at the stated config (BASELINE.json configs[2]): 1024 generators,
+    seeds 1..1024, L=16, full-period de-phasing q=19933, 2^20 words each. The C
+    oracle de-phases every generator with the period-checked x^(2^19933)
+    fixture (make_dephased_states, jump.cpp:35-53, as a polynomial jump) and
+    regenerates its 2^20 words (engine.hpp:92-142); per-generator XOR folds,
+    first 4 and last words go to c3_full.npz, the XOR of all 2^30 words to
+    golden.json. ~40 s of CPU."""
+    o = Oracle()
+    polys = dict(np.load(os.path.join(HERE, "xpow2_full.npz")))
+    t0 = time.time()
+    folds = np.empty(C3_SEEDS, np.uint32)
+    heads = np.empty((C3_SEEDS, 4), np.uint32)
+    lasts = np.empty(C3_SEEDS, np.uint32)
+    for s in range(1, C3_SEEDS + 1):
+        v = o.vmt_stream(o.dephased_states(s, 16, polys["q19933"]), 0, C3_WORDS)
+        folds[s - 1] = np.bitwise_xor.reduce(v)
+        heads[s - 1] = v[:4]
+        lasts[s - 1] = v[-1]
+    np.savez_compressed(os.path.join(HERE, "c3_full.npz"), folds=folds, heads=heads, lasts=lasts)
+    out["c3_full"] = {"lanes": 16, "q": 19933, "seeds": [1, C3_SEEDS], "count_per_gen": C3_WORDS,
+                      "xor": int(np.bitwise_xor.reduce(folds))}
+    print(f"c3 full checksum 0x{out['c3_full']['xor']:08x} {time.time() - t0:.1f}s", flush=True)
+
+
 def main() -> None:
     skip_ladder = "--skip-ladder" in sys.argv
     if "--only" in sys.argv:
@@ -119,7 +148,8 @@ def main() -> None:
         path = os.path.join(HERE, "golden.json")
         with open(path) as f:
             out = json.load(f)
-        {"vmtj": vmtj_section, "stats": stats_section, "c4_full": c4_full_section}[section](RefLib(), out)
+        {"vmtj": vmtj_section, "stats": stats_section, "c4_full": c4_full_section,
+         "c3_full": c3_full_section}[section](RefLib(), out)
         with open(path, "w") as f:
             json.dump(out, f, indent=1)
         return
@@ -199,6 +229,7 @@ def main() -> None:
     vmtj_section(r, out)
     stats_section(r, out)
     c4_full_section(r, out)
+    c3_full_section(r, out)
 
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(out, f, indent=1)

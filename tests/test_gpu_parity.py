@@ -10,7 +10,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import paper_2309_16682_b200 as V  # noqa: E402
-from conftest import dephase_poly  # noqa: E402
+from conftest import dephase_poly, oracle_window  # noqa: E402
 
 
 def sha(a):
@@ -359,12 +359,30 @@ def xor_reduce_inplace(t):
     return int(t[0].item()) & 0xFFFFFFFF
 
 
-def test_bench_workload_pinned_to_oracle(golden):
+# Window offsets into the config-4 stream [0, 2^34): three drawn from a fixed
+# seed, plus windows straddling the rank boundaries of the N=8, 4 and 2 splits
+# (2^31, 2^32, 2^33) and the last 2^20 words (BASELINE.json configs[3]:
+# "2^20-word windows at random offsets against the CPU oracle").
+C4_WIN = 1 << 20
+C4_OFFSETS = sorted([int(v) for v in np.random.default_rng(2309).integers(0, (1 << 34) - C4_WIN, 3)]
+                    + [(1 << 31) - (C4_WIN >> 1), (1 << 32) - 12345, (1 << 33) - (C4_WIN >> 1) + 7,
+                       3 * (1 << 32) - 99, (1 << 34) - C4_WIN])
+
+
+@pytest.fixture(scope="module")
+def c4_oracle_windows(oracle, full_polys):
+    lanes = oracle.dephased_states(5489, 32, full_polys["q19932"])
+    return {s: oracle_window(oracle, 5489, 32, None, s, C4_WIN, dephased=lanes) for s in C4_OFFSETS}
+
+
+def test_bench_workload_pinned_to_oracle(golden, c4_oracle_windows):
     """The bench's config-4 step itself (L=32, seed 5489, full period, words
-    [0, 2^34), 64 GiB): the C oracle's XOR of every word (tests/golden,
-    make_golden.py c4_full) equals both the fused checksum and the XOR of the
-    64 GiB actually stored in HBM; words around the 2^32 boundary and at the
-    end equal an independently positioned generator (64-bit indexing)."""
+    [0, 2^34), 64 GiB), stored in HBM in one call: the C oracle's XOR of every
+    word (tests/golden, make_golden.py c4_full) equals both the fused checksum
+    and the XOR of the 64 GiB actually stored; 2^20-word windows of the stored
+    buffer at random offsets and across the N=2/4/8 rank boundaries equal the
+    C oracle word for word (windows: proj/tests/test_engine.cpp:37-49,
+    acceptance.cpp:222-232)."""
     c = golden["c4_full"]
     n = c["count"]
     g = V.VmtGenerator(c["seed"], V.VmtConfig(c["lanes"]))
@@ -372,15 +390,30 @@ def test_bench_workload_pinned_to_oracle(golden):
     assert g.checksum_xor(n) == c["xor"]
     out = dev_u32(n)
     V.VmtGenerator(c["seed"], V.VmtConfig(c["lanes"])).fill_u32(out)
-    for start in ((1 << 32) - 5, n - 1000, (1 << 33) + 12345):
-        h = V.VmtGenerator(c["seed"], V.VmtConfig(c["lanes"]))
-        h.skip(start)
-        w = dev_u32(1000)
-        h.fill_u32(w)
-        m = min(1000, n - start)
-        assert torch.equal(out[start:start + m].view(torch.int32), w[:m].view(torch.int32)), start
+    for start, ref in c4_oracle_windows.items():
+        assert np.array_equal(host(out[start:start + C4_WIN]), ref), start
     assert xor_reduce_inplace(out) == c["xor"]
     del out
+
+
+@pytest.mark.parametrize("start", C4_OFFSETS)
+def test_config4_full_period_windows_vs_oracle(c4_oracle_windows, start):
+    """Each window again through a generator positioned with skip() -- the way
+    a rank of the N-GPU split positions itself -- in store mode and in the
+    fused-XOR (no-store) mode, against the C oracle at q=19932."""
+    ref = c4_oracle_windows[start]
+    g = V.VmtGenerator(5489, V.VmtConfig(32))
+    g.skip(start)
+    w = dev_u32(C4_WIN)
+    g.fill_u32(w)
+    assert np.array_equal(host(w), ref), start
+    h = V.VmtGenerator(5489, V.VmtConfig(32))
+    h.skip(start)
+    assert h.checksum_xor(C4_WIN) == int(np.bitwise_xor.reduce(ref)), start
+    # the fused path continues exactly where the window ends
+    nxt = dev_u32(1000)
+    g.fill_u32(nxt)
+    assert h.checksum_xor(1000) == int(np.bitwise_xor.reduce(host(nxt)))
 
 
 def test_config1_full_size_vs_oracle(oracle, full_polys):
@@ -413,18 +446,34 @@ def test_config2_full_size_vs_oracle(oracle, full_polys):
     assert np.array_equal(host(t64).view(np.uint64), ref64.view(np.uint64))
 
 
-def test_config3_full_size_every_generator():
+def test_config3_full_size_every_generator(golden, gnpz):
     """c3 as BASELINE.json states it: 1024 generators (seeds 1..1024), L=16,
-    default (full-period) de-phasing, 2^20 words each, generator-major. Every
-    generator's block equals its own single-generator stream (XOR fold and
-    first/last words), the single-generator path being pinned to the oracle."""
+    default (full-period) de-phasing, 2^20 words each, generator-major, in one
+    batch call. Every generator's XOR fold, first 4 and last words equal the C
+    oracle's (tests/golden/c3_full.npz, make_golden.py c3_full), hence the
+    full 2^30-word checksum too."""
     n, ngen = 1 << 20, 1024
+    ref = gnpz("c3_full.npz")
     out = dev_u32(n * ngen)
     V.batch_fill_u32(out, 1, ngen, 16, n)
     v = host(out).reshape(ngen, n)
     folds = np.bitwise_xor.reduce(v, axis=1)
-    for s in range(1, ngen + 1):
-        g = V.VmtGenerator(s, V.VmtConfig(16))
-        head = g.next_block16()
-        assert np.array_equal(v[s - 1, :16], head), s
-        assert g.checksum_xor(n - 16) ^ int(np.bitwise_xor.reduce(head)) == int(folds[s - 1]), s
+    assert np.array_equal(folds, ref["folds"])
+    assert np.array_equal(v[:, :4], ref["heads"]) and np.array_equal(v[:, -1], ref["lasts"])
+    assert int(np.bitwise_xor.reduce(folds)) == golden["c3_full"]["xor"]
+
+
+@pytest.mark.parametrize("seed", [1, 512, 1024])
+def test_config3_sampled_generators_vs_oracle(oracle, full_polys, seed):
+    """Sampled c3 generators at q=19933, all 2^20 words against the C oracle:
+    from the 1024-generator batch (tensor-core de-phasing) and from a single
+    generator (polynomial de-phasing)."""
+    n, ngen = 1 << 20, 1024
+    ref = oracle_window(oracle, seed, 16, full_polys["q19933"], 0, n)
+    out = dev_u32(n * ngen)
+    V.batch_fill_u32(out, 1, ngen, 16, n)
+    assert np.array_equal(host(out[(seed - 1) * n:seed * n]), ref), seed
+    del out
+    w = dev_u32(n)
+    V.VmtGenerator(seed, V.VmtConfig(16)).fill_u32(w)
+    assert np.array_equal(host(w), ref), seed

@@ -194,13 +194,38 @@ def test_dephased_L32_matches_reference(oracle, gnpz):
 
 
 def test_config4_windows_q16(oracle, golden):
+    """The window helper the full-period GPU tests use (conftest.oracle_window)
+    reproduces the reference's own windows (rung composition through
+    jump_state, make_golden.py) at q=16."""
+    from conftest import oracle_window
     lanes = oracle.dephased_states(5489, 32, oracle.x_pow2_mod(16))
     for w in golden["c4_windows_q16"]:
-        b = w["start_word"] // (624 * 32)
-        poly = oracle.x_pow_mod(624 * b)
-        moved = np.stack([oracle.poly_jump(lanes[t], poly) for t in range(32)])
-        v = oracle.vmt_stream(moved, 0, w["count"])
+        v = oracle_window(oracle, 5489, 32, None, w["start_word"], w["count"], dephased=lanes)
         assert sha(v) == w["sha"] and list(v[:8]) == w["head"]
+
+
+def test_oracle_window_unaligned_start(oracle):
+    """oracle_window at a start inside a block equals the plain stream."""
+    from conftest import oracle_window
+    poly = oracle.x_pow2_mod(8)
+    full = oracle.vmt_stream(oracle.dephased_states(7, 16, poly), 0, 5 * 624 * 16 + 3000)
+    for start in (1, 624 * 16 - 1, 3 * 624 * 16 + 17):
+        assert np.array_equal(oracle_window(oracle, 7, 16, poly, start, 3000), full[start:start + 3000])
+
+
+def test_c3_full_fixture_consistent(golden, gnpz):
+    ref = gnpz("c3_full.npz")
+    assert ref["folds"].shape == (1024,) and ref["heads"].shape == (1024, 4)
+    assert int(np.bitwise_xor.reduce(ref["folds"])) == golden["c3_full"]["xor"]
+
+
+
+def test_c3_first_outputs_are_scalar_first_outputs(oracle, gnpz):
+    """Output[0] of every c3 generator is its seed's first scalar MT output
+    (independent of the de-phasing)."""
+    heads = gnpz("c3_full.npz")["heads"]
+    for s in range(1, 1025):
+        assert int(heads[s - 1, 0]) == int(oracle.mt_stream(s, 1)[0]), s
 
 
 def test_config5_jumps_match_reference(oracle, gnpz):
