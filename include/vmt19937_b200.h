@@ -66,6 +66,11 @@ int vmt_create(uint32_t seed, unsigned lanes, unsigned jump_exponent, int device
  * Mt19937::from_words semantics, mt19937.cpp:29-34) as the generator's start. */
 int vmt_create_from_states(const uint32_t* lane_states, unsigned lanes, int device, vmt_handle* out);
 
+/* Copy of a generator (VmtEngine's value semantics, engine.hpp:41-158): an
+ * independent handle with the same lanes, de-phasing and stream position;
+ * both continue with identical words. Waits for src's pending work. */
+int vmt_clone(vmt_handle src, vmt_handle* out);
+
 int vmt_destroy(vmt_handle h);
 
 unsigned vmt_lanes(vmt_handle h);              /* VmtEngine::lanes (engine.hpp:47)          */
@@ -280,6 +285,11 @@ int vmt_chi2_bytes_from_counts(uint64_t count, const uint64_t* bins256, vmt_stat
  * lane t's sequence is column t of the combined stream. Needs lanes >= 2
  * (VMT_EINVAL). Floating point: equal to the reference within 1e-12. */
 int vmt_lane_cross_correlation(vmt_handle h, uint64_t count, vmt_stat_report* out);
+/* The same statistic over caller-supplied words, combined-stream order
+ * (lane t's i-th word at words[i*lanes + t]); host arithmetic. Serves the
+ * reference's lane_cross_correlation(std::vector<WordSource>, count). */
+int vmt_lane_cross_correlation_from_words(const uint32_t* words, unsigned lanes, uint64_t count,
+                                          vmt_stat_report* out);
 /* detail::regularized_gamma_q (stats.hpp:47-50, stats.cpp:52-60). */
 int vmt_regularized_gamma_q(double a, double x, double* out);
 

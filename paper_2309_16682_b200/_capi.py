@@ -19,7 +19,7 @@ VMT_F32_24, VMT_F64_32, VMT_F64_REAL3, VMT_F64_RES53 = 0, 1, 2, 3
 
 # every symbol include/vmt19937_b200.h declares
 EXPORTS = [
-    "vmt_full_period_exponent", "vmt_create", "vmt_create_from_states", "vmt_destroy", "vmt_lanes",
+    "vmt_full_period_exponent", "vmt_create", "vmt_create_from_states", "vmt_clone", "vmt_destroy", "vmt_lanes",
     "vmt_state_words", "vmt_jump_exponent", "vmt_position", "vmt_next_u32", "vmt_next_block16",
     "vmt_next_block_state", "vmt_fill_u32", "vmt_fill_f32", "vmt_fill_f64", "vmt_checksum_xor",
     "vmt_skip", "vmt_seek", "vmt_synchronize", "vmt_export_state", "vmt_batch_fill_u32", "vmt_jump_states", "vmt_seed_states",
@@ -29,6 +29,7 @@ EXPORTS = [
     "vmt_compute_jump_matrix_file", "vmt_vec_mat_mul", "vmt_jump_states_matrix", "vmt_create_from_matrix",
     "vmt_create_from_file", "vmt_stat_counts", "vmt_monobit", "vmt_chi2_bytes", "vmt_regularized_gamma_q",
     "vmt_monobit_from_counts", "vmt_chi2_bytes_from_counts", "vmt_lane_cross_correlation",
+    "vmt_lane_cross_correlation_from_words",
     "vmt_batch_create", "vmt_batch_fill", "vmt_batch_skip", "vmt_batch_position", "vmt_batch_export_state",
     "vmt_batch_destroy", "vmt_multi_gpu_fill", "vmt_store_bandwidth",
     "vmt_set_positioning", "vmt_positioning_stats", "vmt_release_caches",

@@ -90,6 +90,41 @@ void stat_counts(vmt_generator* h, std::uint64_t n, std::uint64_t* c, cudaStream
     h->mark(st);
 }
 
+// lane_cross_correlation's arithmetic (stats.cpp:109-150) over count*m words
+// in combined-stream order (lane t's i-th word at words[i*m + t]).
+void lane_corr(const std::uint32_t* words, unsigned m, std::uint64_t count, vmt_stat_report* out) {
+    std::vector<double> u((std::size_t)(count * m)); // [t][i]
+    for (std::uint64_t i = 0; i < count; ++i)
+        for (unsigned t = 0; t < m; ++t)
+            u[t * count + i] = (double(words[i * m + t]) + 0.5) / 4294967296.0;
+    std::vector<double> mean(m, 0.0), var(m, 0.0);
+    for (unsigned t = 0; t < m; ++t) {
+        const double* x = u.data() + t * count;
+        for (std::uint64_t i = 0; i < count; ++i)
+            mean[t] += x[i];
+        mean[t] /= double(count);
+        for (std::uint64_t i = 0; i < count; ++i)
+            var[t] += (x[i] - mean[t]) * (x[i] - mean[t]);
+    }
+    double max_rho = 0.0;
+    for (unsigned s = 0; s < m; ++s)
+        for (unsigned t = s + 1; t < m; ++t) {
+            const double* a = u.data() + s * count;
+            const double* b = u.data() + t * count;
+            double cov = 0.0;
+            for (std::uint64_t i = 0; i < count; ++i)
+                cov += (a[i] - mean[s]) * (b[i] - mean[t]);
+            const double denom = std::sqrt(var[s] * var[t]);
+            const double rho = denom > 0.0 ? cov / denom : 1.0;
+            max_rho = std::max(max_rho, std::abs(rho));
+        }
+    out->name = "lane_cross_correlation";
+    out->samples = count;
+    out->statistic = max_rho;
+    out->p_value = std::erfc(max_rho * std::sqrt(double(count)) / std::sqrt(2.0));
+    out->pass = max_rho < 4.0 / std::sqrt(double(count));
+}
+
 } // namespace
 
 extern "C" {
@@ -190,36 +225,17 @@ int vmt_lane_cross_correlation(vmt_handle h, uint64_t count, vmt_stat_report* ou
             if (rc != VMT_OK)
                 throw VmtError(rc, g_last_error);
         }
-        std::vector<double> u((std::size_t)(count * m)); // [t][i]
-        for (std::uint64_t i = 0; i < count; ++i)
-            for (unsigned t = 0; t < m; ++t)
-                u[t * count + i] = (double(words[i * m + t]) + 0.5) / 4294967296.0;
-        std::vector<double> mean(m, 0.0), var(m, 0.0);
-        for (unsigned t = 0; t < m; ++t) {
-            const double* x = u.data() + t * count;
-            for (std::uint64_t i = 0; i < count; ++i)
-                mean[t] += x[i];
-            mean[t] /= double(count);
-            for (std::uint64_t i = 0; i < count; ++i)
-                var[t] += (x[i] - mean[t]) * (x[i] - mean[t]);
-        }
-        double max_rho = 0.0;
-        for (unsigned s = 0; s < m; ++s)
-            for (unsigned t = s + 1; t < m; ++t) {
-                const double* a = u.data() + s * count;
-                const double* b = u.data() + t * count;
-                double cov = 0.0;
-                for (std::uint64_t i = 0; i < count; ++i)
-                    cov += (a[i] - mean[s]) * (b[i] - mean[t]);
-                const double denom = std::sqrt(var[s] * var[t]);
-                const double rho = denom > 0.0 ? cov / denom : 1.0;
-                max_rho = std::max(max_rho, std::abs(rho));
-            }
-        out->name = "lane_cross_correlation";
-        out->samples = count;
-        out->statistic = max_rho;
-        out->p_value = std::erfc(max_rho * std::sqrt(double(count)) / std::sqrt(2.0));
-        out->pass = max_rho < 4.0 / std::sqrt(double(count));
+        lane_corr(words.data(), m, count, out);
+    });
+}
+
+int vmt_lane_cross_correlation_from_words(const uint32_t* words, unsigned lanes, uint64_t count,
+                                          vmt_stat_report* out) {
+    return guarded([&] {
+        require(out != nullptr && (words != nullptr || count == 0), VMT_EINVAL, "null argument");
+        if (lanes < 2)
+            throw std::invalid_argument("lane_cross_correlation needs at least 2 lanes");
+        lane_corr(words, lanes, count, out);
     });
 }
 

@@ -1156,6 +1156,29 @@ int vmt_create_from_states(const uint32_t* lane_states, unsigned lanes, int devi
     });
 }
 
+int vmt_clone(vmt_handle src, vmt_handle* out) {
+    return guarded([&] {
+        require(src != nullptr && out != nullptr, VMT_EINVAL, "null argument");
+        DeviceGuard g(src->device);
+        VMT_CUDA(cudaEventSynchronize(src->last)); // every fill / prefetch of src has finished
+        VMT_CUDA(cudaStreamSynchronize(src->own));
+        if (src->side)
+            VMT_CUDA(cudaStreamSynchronize(src->side));
+        std::unique_ptr<vmt_generator> h(new_handle(src->L, src->device));
+        h->q = src->q;
+        const size_t bytes = (size_t)kN * src->L * 4;
+        VMT_CUDA(cudaMemcpy(h->base.p, src->base.p, bytes, cudaMemcpyDeviceToDevice));
+        VMT_CUDA(cudaMemcpy(h->cur.p, src->cur.p, bytes, cudaMemcpyDeviceToDevice));
+        h->cur_block = src->cur_block;
+        h->pos = h->gpos = h->hstage_start = src->pos; // nothing staged: the copy starts at src's position
+        h->max_chunks = src->max_chunks;
+        h->variant = src->variant;
+        h->positioning = src->positioning;
+        h->prefetch = src->prefetch;
+        *out = h.release();
+    });
+}
+
 int vmt_destroy(vmt_handle h) {
     return guarded([&] {
         if (!h)

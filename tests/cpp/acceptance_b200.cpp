@@ -1,5 +1,6 @@
-// Acceptance checks written against the C++ mirror header (include/
-// vmt19937_b200.hpp), in the style of proj/tests/acceptance.cpp: one
+// Acceptance checks of the GPU-only extensions of the reference-compatible
+// C++ headers (include/vmt19937/*.hpp), in the style of
+// proj/tests/acceptance.cpp: one
 // PASS/FAIL line per criterion, exit code = number of failures. Built and run
 // by tests/test_cpp_abi.py (GPU) and compiled (not run) on CPU.
 #include <cstdint>
@@ -9,9 +10,10 @@
 #include <string>
 #include <vector>
 
-#include "vmt19937_b200.hpp"
+#include "vmt19937/engine.hpp"
+#include "vmt19937/jump_file.hpp"
 
-using namespace vmt19937_b200;
+using namespace vmt19937;
 
 namespace {
 
@@ -110,6 +112,33 @@ int main() {
         }
         throw std::runtime_error("no exception");
     });
+    criterion("copies continue identically (VmtEngine value semantics)", [] {
+        VmtEngine<16> a(77, 12);
+        for (int i = 0; i < 12345; ++i)
+            a.next_u32();
+        VmtEngine<16> b = a;
+        for (int i = 0; i < 30000; ++i)
+            require(a.next_u32() == b.next_u32(), "copy diverges at " + std::to_string(i));
+        Mt19937 s(5489);
+        for (int i = 0; i < 700; ++i)
+            s.next_u32();
+        Mt19937 t = s;
+        require(s.cursor() == 76 && t.cursor() == 76, "cursor");
+        for (int i = 0; i < 2000; ++i)
+            require(s.next_u32() == t.next_u32(), "scalar copy diverges at " + std::to_string(i));
+        return std::string("engine and scalar copies");
+    });
+    criterion("interleaved_state() span and state_data() (engine.hpp:100-102)", [] {
+        VmtEngine<8> g(5489, 10);
+        std::span<const std::uint32_t, VmtEngine<8>::state_words> s0 = g.interleaved_state();
+        require(s0[0] == 5489u, "lane 0 word 0 keeps the raw seed before the first query");
+        std::vector<std::uint32_t> blk(VmtEngine<8>::state_words);
+        g.next_block_state(blk.data());
+        const std::uint32_t* p = g.state_data();
+        for (std::size_t i = 0; i < blk.size(); ++i)
+            require(temper(p[i]) == blk[i], "state words temper to the block at " + std::to_string(i));
+        return std::string("state words == untempered block");
+    });
     criterion("bad lane count is invalid_argument (engine.hpp:29-32)", [] {
         try {
             VmtGenerator g(1, VmtConfig(3, QueryMode::kSingle, 4));
@@ -132,7 +161,7 @@ int main() {
         return std::string("0x5E141D5B");
     });
     criterion("full-period default de-phasing starts at the scalar first output", [] {
-        VmtEngine<32> g(5489);
+        VmtEngine<32> g(5489, VMT_FULL_PERIOD);
         require(g.jump_exponent() == 19932, "exponent");
         require(g.next_u32() == 3499211612u, "first output");
         return std::string("q=19932");
@@ -141,7 +170,10 @@ int main() {
         const unsigned q = 10;
         const F2Matrix B = jump_matrix_pow2(q);
         const std::string path = "/tmp/acceptance_b200_" + jump_matrix_file_name(q);
-        compute_jump_matrix(q, path);
+        JumpComputeOptions opt;
+        opt.exponent = q;
+        opt.out = path;
+        compute_jump_matrix(opt);
         const LoadedJumpMatrix m = read_jump_matrix_file(path);
         std::remove(path.c_str());
         require(m.exponent == q && m.matrix == B, "file round trip");

@@ -1,37 +1,103 @@
-"""The C++ mirror header (include/vmt19937_b200.hpp) over the C ABI:
-tests/cpp/acceptance_b200.cpp compiles against it on CPU and passes every
-criterion on the GPU."""
+"""The reference-compatible C++ headers (include/vmt19937/*.hpp) over the C
+ABI, proven with the reference's own callers: tests/cpp/Makefile compiles
+/root/reference/proj/tests/acceptance.cpp and proj/src/bench.cpp UNCHANGED
+against them (only the include root differs), plus our acceptance_b200.cpp
+for the GPU-only extensions. On CPU the programs build and link; on the B200
+they run and must pass (the binaries are built here, where /root/reference
+exists, and travel to the GPU box in tests/cpp/_build/)."""
+import csv
+import io
 import os
 import shutil
 import subprocess
 
+import numpy as np
 import pytest
 
 from conftest import ROOT
 
-SRC = os.path.join(ROOT, "tests", "cpp", "acceptance_b200.cpp")
-LIBDIR = os.path.join(ROOT, "paper_2309_16682_b200")
+CPP = os.path.join(ROOT, "tests", "cpp")
+OUT = os.path.join(CPP, "_build")
+REF = "/root/reference/proj"
 
 
-def build(out):
-    gxx = shutil.which("g++")
-    if gxx is None:
-        pytest.skip("g++ unavailable")
-    cmd = [gxx, "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"), SRC, "-L", LIBDIR,
-           "-l:libvmt19937_b200.so", f"-Wl,-rpath,{LIBDIR}", "-o", out]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    assert r.returncode == 0, r.stderr
-    return out
+def make():
+    if shutil.which("g++") is None or shutil.which("make") is None:
+        pytest.skip("g++/make unavailable")
+    r = subprocess.run(["make", "-C", CPP, "all"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
 
 
-def test_cpp_header_compiles(tmp_path):
-    build(str(tmp_path / "acc"))
+def exe(name):
+    path = os.path.join(OUT, name)
+    if not os.path.exists(path):
+        make()
+    assert os.path.exists(path), f"{path} missing: build it with `make -C tests/cpp` where /root/reference exists"
+    return path
+
+
+def test_headers_compile_reference_callers():
+    """acceptance.cpp and bench.cpp from the reference compile and link
+    against include/vmt19937 (this container has the reference)."""
+    if not os.path.isdir(REF):
+        pytest.skip("reference sources absent (GPU box)")
+    make()
+    for name in ("ref_acceptance", "ref_bench", "acceptance_b200"):
+        assert os.path.exists(os.path.join(OUT, name)), name
+
+
+def test_headers_are_self_contained(tmp_path):
+    """Every public header compiles on its own (C++20)."""
+    inc = os.path.join(ROOT, "include", "vmt19937")
+    for h in sorted(os.listdir(inc)):
+        if not h.endswith(".hpp"):
+            continue
+        src = tmp_path / f"{h}.cpp"
+        src.write_text(f'#include "vmt19937/{h}"\nint main() {{ return 0; }}\n')
+        r = subprocess.run(["g++", "-std=c++20", "-Wall", "-Werror", "-fsyntax-only", "-I",
+                            os.path.join(ROOT, "include"), str(src)], capture_output=True, text=True)
+        assert r.returncode == 0, h + "\n" + r.stderr
 
 
 @pytest.mark.gpu
-def test_cpp_acceptance_on_gpu(tmp_path):
-    exe = build(str(tmp_path / "acc"))
-    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+def test_reference_acceptance_on_gpu():
+    """The reference's acceptance suite, unchanged, driving the GPU engines:
+    every criterion passes (the two CPU-SIMD throughput-ratio criteria report
+    instead of asserting, because has_simd_lanes<N>() is false here)."""
+    r = subprocess.run([exe("ref_acceptance")], capture_output=True, text=True, timeout=1200)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "acceptance: 9/9 criteria passed" in r.stdout
+
+
+@pytest.mark.gpu
+def test_reference_bench_checksums_on_gpu(golden, oracle):
+    """The reference's run_benchmark (bench.cpp, unchanged) over the GPU
+    engines: the checksum of every lane count and query mode equals the
+    reference CPU library's (golden bench_checksums, q=6, 10^6 words, seed
+    5489) and the C oracle's; the scalar generator's equals the scalar MT
+    stream's."""
+    r = subprocess.run([exe("ref_bench"), "1000000", "6"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    rows = list(csv.DictReader(io.StringIO(r.stdout)))
+    assert len(rows) == 16
+    want = {(g["lanes"], g["mode"]): g["xor"] for g in golden["bench_checksums"]}
+    for row in rows:
+        x = int(row["checksum"], 16)
+        if row["lanes"] == "scalar":
+            assert x == int(np.bitwise_xor.reduce(oracle.mt_stream(5489, 1000000)))
+            continue
+        L, m = int(row["lanes"]), int(row["mode"])
+        if (L, m) in want:
+            assert x == want[(L, m)], row
+        else:
+            lanes = oracle.dephased_states(5489, L, oracle.x_pow2_mod(6))
+            assert x == oracle.vmt_checksum(lanes, 0, 1000000), row
+
+
+@pytest.mark.gpu
+def test_cpp_extensions_acceptance_on_gpu():
+    r = subprocess.run([exe("acceptance_b200")], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failure(s)" in r.stdout
