@@ -408,7 +408,6 @@ def main():
     ms = e0.elapsed_time(e1) / args.steps
     ms = max_over_ranks(ms, coll)
     launches = sum(s1[k] - s0[k] for k in ("gen_launches", "jump_launches", "other_launches"))
-    # (the positioning GEMM is cuBLAS's kernel and is not counted)
     # the generation kernel's own duration and the positioning jumps before
     # it, from the same timed steps
     gen_ms = max_over_ranks(gen_tot / max(fills, 1), coll)
@@ -437,7 +436,7 @@ def main():
         serial = {"ms_per_step": f0.elapsed_time(f1) / 3, "gen_kernel": sg / max(sf, 1),
                   "positioning": sj / max(sf, 1),
                   "gen_roofline_frac": count * 4 / (sg / max(sf, 1) * 1e-3) / 1e9 / measured_peak()[0],
-                  "note": "3 steps with vmt_set_prefetch(OFF): one cuBLASLt FP4 GEMM between steps instead"}
+                  "note": "3 steps with vmt_set_prefetch(OFF): our tcgen05 FP4 GEMM between steps instead"}
 
     # -- global checksum of one full 2^34 range (config 4 verification)
     g.seek(start)
@@ -558,7 +557,7 @@ def main():
                                         "chunk lane states are computed during this step's generation kernel by the "
                                         "co-resident tcgen05 FP4 GEMM (vmt_posmma_kernel, on the idle tensor cores), "
                                         "so 'positioning' is only the wait for it and its cost shows up inside "
-                                        "gen_kernel; first steps: polynomial jumps, then the serial cuBLASLt FP4 GEMM"},
+                                        "gen_kernel; first steps: polynomial jumps, then the serial tcgen05 FP4 GEMM"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": (traffic or {}).get("dram_bytes_per_launch"),
                      "kernel": "vmt_gen_kernel", "peak_source": peak_src,

@@ -229,8 +229,8 @@ int vmt_set_tuning(vmt_handle h, unsigned max_chunks, int variant);
 int vmt_set_prefetch(vmt_handle h, int enable);
 
 /* Chunk positioning of consecutive fills: mode 0 =
- * auto (one FP4 tensor-core GEMM -- our tcgen05 kernel, cuBLASLt below 2048
- * rows -- maps the previous fill's chunk states to the next fill's when the
+ * auto (one FP4 tensor-core GEMM -- our tcgen05 kernel -- maps the previous
+ * fill's chunk states to the next fill's when the
  * fill shape and block delta repeat and there are at least 1024 lane states;
  * polynomial jumps otherwise), 1 = polynomial jumps only, 2 = GEMM whenever
  * the shape repeats. Results are identical. */

@@ -242,6 +242,8 @@ class VmtGenerator:
         addr, keep, size, kind = _ptr(out)
         _check_dtype(out, np.float32, "float32")
         n = size if n is None else n
+        if n > size:
+            raise InvalidArgument(_capi.VMT_EINVAL, "n exceeds buffer size")
         check(lib.vmt_fill_f32(self._h, addr, n, rule, _stream_for(kind, stream)))
         return out
 
@@ -249,6 +251,8 @@ class VmtGenerator:
         addr, keep, size, kind = _ptr(out)
         _check_dtype(out, np.float64, "float64")
         n = size if n is None else n
+        if n > size:
+            raise InvalidArgument(_capi.VMT_EINVAL, "n exceeds buffer size")
         check(lib.vmt_fill_f64(self._h, addr, n, rule, _stream_for(kind, stream)))
         return out
 

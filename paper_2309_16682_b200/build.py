@@ -73,9 +73,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             errs.append(" ".join(p.args) + "\n" + o)
     if errs:
         raise RuntimeError("nvcc failed:\n" + "\n".join(errs))
-    cudalib = os.path.join(os.path.dirname(os.path.dirname(os.path.realpath(_nvcc()))), "lib64")
-    link = [_nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", LIB + ".tmp", *[o for _, o in jobs], "-lpthread",
-            "-lcublas", "-lcublasLt", "-Xlinker", "-rpath", "-Xlinker", cudalib]
+    # no CUDA library beyond the statically linked runtime: every kernel is ours
+    link = [_nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", LIB + ".tmp", *[o for _, o in jobs], "-lpthread"]
     if verbose:
         print(" ".join(link), flush=True)
     out = subprocess.run(link, capture_output=True, text=True)

@@ -8,17 +8,13 @@
 //   new[C*L][19968] = old[C*L][19968] x F^(624 D)[19968][19968]  (mod 2)
 // in word-bit coordinates (vmt_matrix.cuh) with FP4 e2m1 0/1 operands, unit
 // block scales and fp32 accumulation (exact: sums <= 19937):
-//   * our tcgen05 kernels (vmt_posmma.cuh): the CTA-pair kernel, from 2048
-//     lane states on -- serially between fills, or co-resident with the
-//     generation kernel as the prefetch of the next fill (VMT_PREFETCH_TENSOR);
-//   * cuBLASLt's block-scaled FP4 GEMM between our operand and packing
-//     kernels (small row counts, and the fallback), else int8 x int8 -> int32
-//     where the library has no FP4 kernel.
+// our own tcgen05 kernels (vmt_posmma.cuh; no cuBLAS) -- serially between
+// fills, or co-resident with the generation kernel as the prefetch of the
+// next fill (VMT_PREFETCH_TENSOR). Where the kernel cannot be set up (no TMA
+// descriptor encoder) the caller falls back to the polynomial jumps.
 // The 200 MB FP4 matrix for a delta is built once (19937 basis jumps +
 // expansion) when the delta repeats; two are cached, and deltas up to 4 blocks
 // above a cached one reuse it (the rest regenerated in place).
-#include <cublasLt.h>
-#include <cublas_v2.h>
 #include <cudaTypedefs.h>
 
 #ifndef VMT_GEMM_MIN_ROWS
@@ -37,105 +33,20 @@ inline std::uint64_t gemm_min_rows() {
 constexpr std::size_t kGemmMatBytes = (std::size_t)kWB * kWB;
 
 struct GemmPos {
-    cublasHandle_t blas = nullptr;
-    cublasLtHandle_t lt = nullptr;
-    int fp4 = -1; // -1 untried, 0 unavailable (int8 path), 1 in use
-    DevBuf<std::uint8_t> scale_a, scale_b; // unit e4m3 block scales
-    DevBuf<std::uint8_t> work;
-    std::uint64_t scale_rows = 0;
-    std::map<std::uint64_t, std::unique_ptr<DevBuf<std::int8_t>>> mats; // delta -> F^(624 delta), word-bit
+    std::map<std::uint64_t, std::unique_ptr<DevBuf<std::int8_t>>> mats; // delta -> F^(624 delta), FP4 word-bit
     // TMA descriptors of the FP4 matrices (B operand of vmt_posmma_kernel)
     std::map<std::uint64_t, CUtensorMap> tmaps;
     std::map<std::uint64_t, CUtensorMap> tmaps2; // 104-row boxes for the CTA-pair kernel
-    DevBuf<std::int8_t> pm_a; // FP4 state operand of the co-resident prefetch
+    DevBuf<std::int8_t> pm_a; // FP4 state operand
     CUtensorMap pm_tmap_a;
     const void* pm_tmap_ptr = nullptr;
     std::uint64_t pm_tmap_rows = 0;
     std::map<std::uint64_t, std::uint64_t> last_use;                     // delta -> tick of its last use
     std::map<std::uint64_t, int> seen;                                   // delta -> transitions observed
     std::uint64_t tick = 0;
-    DevBuf<std::int8_t> a;
-    DevBuf<std::int32_t> prod;
     bool last_valid = false;
     std::uint64_t last_b0 = 0, last_B = 0, last_C = 0;
-    ~GemmPos() {
-        if (blas)
-            cublasDestroy(blas);
-        if (lt)
-            cublasLtDestroy(lt);
-    }
 };
-
-#define VMT_CUBLAS(x)                                                                                 \
-    do {                                                                                              \
-        cublasStatus_t s_ = (x);                                                                      \
-        if (s_ != CUBLAS_STATUS_SUCCESS)                                                              \
-            throw VmtError(VMT_ECUDA, std::string(#x) + ": cuBLAS status " + std::to_string((int)s_));  \
-    } while (0)
-
-// D[r][j] (fp32) = sum_i bits[r][i] * M[i][j] with FP4 operands; false when
-// cuBLASLt has no FP4 kernel for the shape (caller falls back to int8).
-bool lt_fp4_gemm(GemmPos& gp, const void* mat, const void* bits, float* prod, std::uint64_t rows, cudaStream_t st) {
-    if (!gp.lt && cublasLtCreate(&gp.lt) != CUBLAS_STATUS_SUCCESS)
-        return false;
-    const std::uint64_t kk = kWB, mm = kWB, nn = rows;
-    // unit scales, one e4m3 byte per 16 elements (swizzled layout is irrelevant
-    // when every scale is 1.0): A covers mm x kk, B covers nn x kk
-    if (gp.scale_rows < rows) {
-        gp.scale_a.reserve(mm * (kk / 16));
-        gp.scale_b.reserve(nn * (kk / 16));
-        VMT_CUDA(cudaMemsetAsync(gp.scale_a.p, 0x38, mm * (kk / 16), st));
-        VMT_CUDA(cudaMemsetAsync(gp.scale_b.p, 0x38, nn * (kk / 16), st));
-        gp.scale_rows = rows;
-    }
-    cublasLtMatmulDesc_t op = nullptr;
-    cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
-    cublasLtMatmulPreference_t pref = nullptr;
-    bool ok = false;
-    do {
-        if (cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32F, CUDA_R_32F) != CUBLAS_STATUS_SUCCESS)
-            break;
-        const cublasOperation_t ta = CUBLAS_OP_T, tb = CUBLAS_OP_N;
-        const cublasLtMatmulMatrixScale_t sm = CUBLASLT_MATMUL_MATRIX_SCALE_VEC16_UE4M3;
-        const void* spa = gp.scale_a.p;
-        const void* spb = gp.scale_b.p;
-        cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &ta, sizeof(ta));
-        cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &tb, sizeof(tb));
-        cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_A_SCALE_MODE, &sm, sizeof(sm));
-        cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_B_SCALE_MODE, &sm, sizeof(sm));
-        cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_A_SCALE_POINTER, &spa, sizeof(spa));
-        cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_B_SCALE_POINTER, &spb, sizeof(spb));
-        if (cublasLtMatrixLayoutCreate(&la, CUDA_R_4F_E2M1, kk, mm, kk) != CUBLAS_STATUS_SUCCESS ||
-            cublasLtMatrixLayoutCreate(&lb, CUDA_R_4F_E2M1, kk, nn, kk) != CUBLAS_STATUS_SUCCESS ||
-            cublasLtMatrixLayoutCreate(&lc, CUDA_R_32F, mm, nn, mm) != CUBLAS_STATUS_SUCCESS)
-            break;
-        const std::size_t ws = 64ull << 20;
-        gp.work.reserve(ws);
-        if (cublasLtMatmulPreferenceCreate(&pref) != CUBLAS_STATUS_SUCCESS)
-            break;
-        cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &ws, sizeof(ws));
-        cublasLtMatmulHeuristicResult_t heur{};
-        int found = 0;
-        if (cublasLtMatmulAlgoGetHeuristic(gp.lt, op, la, lb, lc, lc, pref, 1, &heur, &found) !=
-                CUBLAS_STATUS_SUCCESS ||
-            found == 0)
-            break;
-        const float one = 1.f, zero = 0.f;
-        ok = cublasLtMatmul(gp.lt, op, &one, mat, la, bits, lb, &zero, prod, lc, prod, lc, &heur.algo, gp.work.p, ws,
-                            st) == CUBLAS_STATUS_SUCCESS;
-    } while (false);
-    if (pref)
-        cublasLtMatmulPreferenceDestroy(pref);
-    if (la)
-        cublasLtMatrixLayoutDestroy(la);
-    if (lb)
-        cublasLtMatrixLayoutDestroy(lb);
-    if (lc)
-        cublasLtMatrixLayoutDestroy(lc);
-    if (op)
-        cublasLtMatmulDescDestroy(op);
-    return ok;
-}
 
 // TMA descriptor of a K-major FP4 operand [rows][19968 elements = 9984 B]:
 // boxes of 64 B (128 elements) x box_rows rows, 64-byte swizzle.
@@ -176,7 +87,7 @@ bool posmma_launch(GemmPos& gp, std::uint64_t delta, const std::uint32_t* src, s
                    std::uint64_t rows, int sms, cudaStream_t st) {
     const bool pair = posmma_pair();
     auto it = (pair ? gp.tmaps2 : gp.tmaps).find(delta);
-    if (gp.fp4 != 1 || it == (pair ? gp.tmaps2 : gp.tmaps).end() || !gp.mats.count(delta))
+    if (it == (pair ? gp.tmaps2 : gp.tmaps).end() || !gp.mats.count(delta))
         return false;
     gp.last_use[delta] = gp.tick;
     return posmma_run(gp, it->second, src, dst, L, rows, sms, st, L, 0);
@@ -233,21 +144,16 @@ bool posmma_run(GemmPos& gp, const CUtensorMap& tmap_b, const std::uint32_t* src
     return true;
 }
 
-// p(F) in word-bit coordinates as the GEMM's A operand: FP4 ([out][in], two
-// per byte) or int8.
-void build_gemm_matrix(const Poly& poly, bool fp4, DevBuf<std::int8_t>& m, cudaStream_t st) {
+// p(F) in word-bit coordinates as the GEMM's B operand: FP4 [out][in], two
+// elements per byte.
+void build_gemm_matrix(const Poly& poly, DevBuf<std::int8_t>& m, cudaStream_t st) {
     DevBuf<std::uint64_t> rows;
     rows.reserve(kMatWords);
     Counters cnt;
     matrix_from_poly(poly, rows.p, st, cnt);
-    if (fp4) {
-        m.reserve(kGemmMatBytes / 2);
-        vmt_gemm_matrix_fp4_kernel<<<dim3((kWB / 2 + 255) / 256, kWB), 256, 0, st>>>(
-            rows.p, reinterpret_cast<std::uint8_t*>(m.p));
-    } else {
-        m.reserve(kGemmMatBytes);
-        vmt_gemm_matrix_kernel<<<dim3((kWB + 255) / 256, kWB), 256, 0, st>>>(rows.p, m.p);
-    }
+    m.reserve(kGemmMatBytes / 2);
+    vmt_gemm_matrix_fp4_kernel<<<dim3((kWB / 2 + 255) / 256, kWB), 256, 0, st>>>(
+        rows.p, reinterpret_cast<std::uint8_t*>(m.p));
     VMT_CUDA(cudaGetLastError());
     VMT_CUDA(cudaStreamSynchronize(st)); // rows is released on return
 }
@@ -282,13 +188,13 @@ const std::int8_t* gemm_matrix(vmt_generator* h, GemmPos& gp, std::uint64_t delt
     Gf2Field& F = Gf2Field::instance();
     const unsigned __int128 d = (unsigned __int128)kN * delta;
     std::unique_ptr<DevBuf<std::int8_t>> m(new DevBuf<std::int8_t>());
-    build_gemm_matrix(F.x_pow128((std::uint64_t)d, (std::uint64_t)(d >> 64)), gp.fp4 == 1, *m, st);
+    build_gemm_matrix(F.x_pow128((std::uint64_t)d, (std::uint64_t)(d >> 64)), *m, st);
     h->cnt.other += 1;
     const std::int8_t* p = m->p;
     CUtensorMap tm;
-    if (gp.fp4 == 1 && make_tmap_fp4(tm, p, kWB, kPmNH))
+    if (make_tmap_fp4(tm, p, kWB, kPmNH))
         gp.tmaps[delta] = tm;
-    if (gp.fp4 == 1 && make_tmap_fp4(tm, p, kWB, kP2BQ))
+    if (make_tmap_fp4(tm, p, kWB, kP2BQ))
         gp.tmaps2[delta] = tm;
     gp.mats[delta] = std::move(m);
     gp.last_use[delta] = gp.tick;
@@ -342,79 +248,14 @@ bool gemm_position(vmt_generator* h, GemmPos& gp, const std::uint32_t* src, std:
 bool gemm_position_exact(vmt_generator* h, GemmPos& gp, const std::uint32_t* src, std::uint32_t* dst,
                          std::uint64_t rows, std::uint64_t delta, cudaStream_t st) {
     ++gp.tick;
-    static const bool no_fp4 = std::getenv("VMT_GEMM_INT8") != nullptr;
-    if (gp.fp4 < 0 && no_fp4)
-        gp.fp4 = 0;
-    if (gp.fp4 != 0) {
-        // FP4 path (probe on first use; a failure switches to int8 for good)
-        if (gp.fp4 < 0)
-            gp.fp4 = 1;
-        const std::int8_t* mat = gemm_matrix(h, gp, delta, st);
-        if (!mat)
-            return false;
-        // from 2048 lane states on, our tcgen05 CTA-pair kernel (operand
-        // expansion + GEMM + packing epilogue: 0.81 vs 0.85 ms for 4736
-        // states) instead of cuBLASLt's GEMM between our expand and pack
-        // kernels (378 MB fp32 product); below that cuBLASLt's tiles balance
-        // better (config 1, 1200 states: 0.366 vs 0.375 ms per fill)
-        static const bool lt_only = std::getenv("VMT_POSITION_CUBLASLT") != nullptr;
-        if (!lt_only && rows >= 2048 &&
-            posmma_launch(gp, delta, src, dst, h->L, rows, device_info(h->device).sms, st)) {
-            h->cnt.other += 2;
-            h->cnt.gemm_positionings += 1;
-            return true;
-        }
-        const long long nwords = (long long)rows * kN;
-        const unsigned grid = (unsigned)((nwords + 255) / 256);
-        // the block-scale layout tiles rows by 128: pad the state operand with
-        // zero rows to a multiple of 128
-        const std::uint64_t rows_pad = (rows + 127) / 128 * 128;
-        gp.a.reserve(rows_pad * kWB / 2);
-        gp.prod.reserve(rows_pad * kWB);
-        if (rows_pad > rows)
-            VMT_CUDA(cudaMemsetAsync(gp.a.p + rows * kWB / 2, 0, (rows_pad - rows) * kWB / 2, st));
-        vmt_states_to_fp4_kernel<<<grid, 256, 0, st>>>(src, (int)h->L, 0, (int)h->L, nwords,
-                                                        reinterpret_cast<std::uint8_t*>(gp.a.p));
-        VMT_CUDA(cudaGetLastError());
-        float* prod = reinterpret_cast<float*>(gp.prod.p);
-        if (lt_fp4_gemm(gp, mat, gp.a.p, prod, rows_pad, st)) {
-            vmt_f32_to_states_kernel<<<grid, 256, 0, st>>>(prod, (int)h->L, 0, (int)h->L, nwords, dst);
-            VMT_CUDA(cudaGetLastError());
-            h->cnt.other += 2; // expand + pack (the GEMM itself is cuBLASLt's kernel)
-            h->cnt.gemm_positionings += 1;
-            return true;
-        }
-        // no FP4 kernel: drop the FP4 matrices and use int8 from now on
-        VMT_CUDA(cudaStreamSynchronize(st));
-        gp.fp4 = 0;
-        gp.mats.clear();
-        gp.tmaps.clear();
-        gp.tmaps2.clear();
-        gp.last_use.clear();
-    }
-    const std::int8_t* mat = gemm_matrix(h, gp, delta, st);
-    if (!mat)
+    if (!gemm_matrix(h, gp, delta, st))
         return false;
-    if (!gp.blas)
-        VMT_CUBLAS(cublasCreate(&gp.blas));
-    VMT_CUBLAS(cublasSetStream(gp.blas, st));
-    gp.a.reserve(rows * kWB);
-    gp.prod.reserve(rows * kWB);
-    const long long nwords = (long long)rows * kN;
-    const unsigned grid = (unsigned)((nwords + 255) / 256);
-    vmt_states_to_i8_kernel<<<grid, 256, 0, st>>>(src, (int)h->L, nwords, gp.a.p);
-    VMT_CUDA(cudaGetLastError());
-    // In cuBLAS's column-major terms: C (m = 19968 output bits, n = rows) =
-    // A^T (m x k) * B (k x n) with A = mat stored [out j][in i] (lda = k),
-    // B = the state bits stored [row r][in i] (ldb = k), C = prod stored
-    // [row r][out j] (ldc = m): prod[r][j] = sum_i bits[r][i] * M[i][j].
-    const std::int32_t one = 1, zero = 0;
-    VMT_CUBLAS(cublasGemmEx(gp.blas, CUBLAS_OP_T, CUBLAS_OP_N, kWB, (int)rows, kWB, &one, mat, CUDA_R_8I, kWB,
-                            gp.a.p, CUDA_R_8I, kWB, &zero, gp.prod.p, CUDA_R_32I, kWB, CUBLAS_COMPUTE_32I,
-                            CUBLAS_GEMM_DEFAULT));
-    vmt_i32_to_states_kernel<<<grid, 256, 0, st>>>(gp.prod.p, (int)h->L, nwords, dst);
-    VMT_CUDA(cudaGetLastError());
-    h->cnt.other += 2; // expand + pack (the GEMM itself is cuBLAS's kernel)
+    // our tcgen05 kernel at every row count: operand expansion + GEMM with a
+    // packing epilogue (config 1's 1200 states: 0.375 ms per fill; the
+    // bench's 4736: 0.81 ms)
+    if (!posmma_launch(gp, delta, src, dst, h->L, rows, device_info(h->device).sms, st))
+        return false;
+    h->cnt.other += 2;
     h->cnt.gemm_positionings += 1;
     return true;
 }
@@ -425,10 +266,9 @@ bool gemm_position_exact(vmt_generator* h, GemmPos& gp, const std::uint32_t* src
 // (device, q, s), instead of ngen*(L-1) polynomial jumps.
 struct DephaseGemm {
     std::mutex mu;
-    GemmPos gp; // cuBLASLt handle, scales, workspace, operand buffers
+    GemmPos gp; // operand buffer and its TMA descriptor
     std::map<std::pair<unsigned, unsigned>, std::unique_ptr<DevBuf<std::int8_t>>> mats;
     std::map<std::pair<unsigned, unsigned>, CUtensorMap> tmaps; // for vmt_posmma(2)_kernel
-    bool fp4_ok = true;
 };
 
 std::mutex g_dephase_mu;
@@ -443,16 +283,13 @@ DephaseGemm& dephase_gemm(int dev) {
 }
 
 // states: [ngen][624][L], lane 0 seeded; fills lanes 1..L-1. false: not done
-// (no FP4 GEMM here; the caller uses the polynomial jumps).
+// (no TMA descriptor encoder; the caller uses the polynomial jumps).
 bool dephase_by_gemm(int device, cudaStream_t st, unsigned ngen, unsigned L, unsigned q, std::uint32_t* states,
                      Counters& cnt) {
-    static const bool off = std::getenv("VMT_GEMM_INT8") != nullptr; // FP4 only here
-    if (off || L < 2)
+    if (L < 2)
         return false;
     DephaseGemm& D = dephase_gemm(device);
     std::lock_guard<std::mutex> lk(D.mu);
-    if (!D.fp4_ok)
-        return false;
     Gf2Field& F = Gf2Field::instance();
     for (unsigned s = 1; s < L; s *= 2) {
         const unsigned n = std::min(s, L - s);
@@ -465,42 +302,24 @@ bool dephase_by_gemm(int device, cudaStream_t st, unsigned ngen, unsigned L, uns
                 D.tmaps.clear();
             }
             std::unique_ptr<DevBuf<std::int8_t>> m(new DevBuf<std::int8_t>());
-            build_gemm_matrix(F.powmod(F.x_pow2(q), s), true, *m, st);
+            build_gemm_matrix(F.powmod(F.x_pow2(q), s), *m, st);
             cnt.other += 1;
             CUtensorMap tm;
-            if (make_tmap_fp4(tm, m->p, kWB, posmma_pair() ? kP2BQ : kPmNH))
-                D.tmaps[key] = tm;
+            if (!make_tmap_fp4(tm, m->p, kWB, posmma_pair() ? kP2BQ : kPmNH)) {
+                if (s == 1)
+                    return false; // nothing written yet: the caller jumps instead
+                throw VmtError(VMT_ECUDA, "TMA descriptor failed during de-phasing");
+            }
+            D.tmaps[key] = tm;
             it = D.mats.emplace(key, std::move(m)).first;
         }
-        const std::uint64_t rows = (std::uint64_t)ngen * n, rows_pad = (rows + 127) / 128 * 128;
-        // our tcgen05 kernel: lanes [s, s+n) written straight from the
-        // accumulators (no fp32 product pass)
-        static const bool lt_only = std::getenv("VMT_POSITION_CUBLASLT") != nullptr;
-        auto tm = D.tmaps.find(key);
-        if (!lt_only && tm != D.tmaps.end() && rows >= 2048 &&
-            posmma_run(D.gp, tm->second, states, states, L, rows, device_info(device).sms, st, n, s)) {
-            cnt.other += 2;
-            continue;
-        }
-        const long long nwords = (long long)rows * kN;
-        const unsigned grid = (unsigned)((nwords + 255) / 256);
-        D.gp.a.reserve(rows_pad * kWB / 2);
-        D.gp.prod.reserve(rows_pad * kWB);
-        if (rows_pad > rows)
-            VMT_CUDA(cudaMemsetAsync(D.gp.a.p + rows * kWB / 2, 0, (rows_pad - rows) * kWB / 2, st));
-        vmt_states_to_fp4_kernel<<<grid, 256, 0, st>>>(states, (int)L, 0, (int)n, nwords,
-                                                        reinterpret_cast<std::uint8_t*>(D.gp.a.p));
-        VMT_CUDA(cudaGetLastError());
-        float* prod = reinterpret_cast<float*>(D.gp.prod.p);
-        if (!lt_fp4_gemm(D.gp, it->second->p, D.gp.a.p, prod, rows_pad, st)) {
-            D.fp4_ok = false;
-            VMT_CUDA(cudaStreamSynchronize(st));
+        // lanes [s, s+n) of every generator written straight from the accumulators
+        const std::uint64_t rows = (std::uint64_t)ngen * n;
+        if (!posmma_run(D.gp, D.tmaps.at(key), states, states, L, rows, device_info(device).sms, st, n, s)) {
             if (s == 1)
-                return false; // nothing written yet: the caller jumps instead
-            throw VmtError(VMT_ECUDA, "FP4 GEMM failed during de-phasing");
+                return false;
+            throw VmtError(VMT_ECUDA, "positioning GEMM failed during de-phasing");
         }
-        vmt_f32_to_states_kernel<<<grid, 256, 0, st>>>(prod, (int)L, (int)s, (int)n, nwords, states);
-        VMT_CUDA(cudaGetLastError());
         cnt.other += 2;
     }
     VMT_CUDA(cudaStreamSynchronize(st));

@@ -154,13 +154,17 @@ bool posmma_fits(int dev, GenFn fn, int nt, int smem, int per_sm) {
     VMT_CUDA(cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
     VMT_CUDA(cudaDeviceGetAttribute(&sm_regs, cudaDevAttrMaxRegistersPerMultiprocessor, dev));
     VMT_CUDA(cudaDeviceGetAttribute(&sm_threads, cudaDevAttrMaxThreadsPerMultiProcessor, dev));
+    // the positioning kernel posmma_run launches: the CTA pair unless VMT_POSMMA_SINGLE
+    const bool single = std::getenv("VMT_POSMMA_SINGLE") != nullptr;
+    const void* pk = single ? reinterpret_cast<const void*>(vmt_posmma_kernel)
+                            : reinterpret_cast<const void*>(vmt_posmma2_kernel);
+    const int pm_smem = single ? kPmSmem : kP2Smem;
     cudaFuncAttributes ga{}, pa{};
     VMT_CUDA(cudaFuncGetAttributes(&ga, reinterpret_cast<const void*>(fn)));
-    VMT_CUDA(cudaFuncGetAttributes(&pa, reinterpret_cast<const void*>(vmt_posmma_kernel)));
+    VMT_CUDA(cudaFuncGetAttributes(&pa, pk));
     auto regs = [](int per_thread, int threads) { // allocation unit: 256 registers per warp
         return ((per_thread * 32 + 255) / 256 * 256) * ((threads + 31) / 32);
     };
-    const int pm_smem = std::getenv("VMT_POSMMA_SINGLE") ? kPmSmem : kP2Smem; // the kernel posmma_run launches
     const bool ok = per_sm * (smem + 1024) + pm_smem + 1024 <= sm_smem &&
                     per_sm * regs(ga.numRegs, nt) + regs(pa.numRegs, kPmThreads) <= sm_regs &&
                     per_sm * nt + kPmThreads <= sm_threads && !std::getenv("VMT_NO_TC_PREFETCH");
@@ -170,8 +174,7 @@ bool posmma_fits(int dev, GenFn fn, int nt, int smem, int per_sm) {
         // would have no room left for the GEMM CTA
         VMT_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                       cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        VMT_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(vmt_posmma_kernel),
-                                      cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        VMT_CUDA(cudaFuncSetAttribute(pk, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     }
     memo[key] = ok;
     return ok;
@@ -856,6 +859,22 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     p.out_chunk_stride = 0;
     p.blocks_per_chunk = (unsigned)B;
     p.lanes = h->L;
+    // Everything of the prefetch that can free device memory (growing the
+    // alternate chunk buffer, evicting a cached skip polynomial: cudaFree
+    // waits for the whole device) happens before the generation kernel is
+    // queued, so it never serialises the prefetch behind the generation.
+    const std::uint64_t* pref_dp = nullptr;
+    if (prefetch_now) {
+        try {
+            h->chunks_alt.reserve((size_t)C * kN * h->L);
+            if (!tc_pref)
+                pref_dp = skip_poly(h, next_b0 - b0);
+        } catch (const VmtError&) { // e.g. no memory: generate without prefetching
+            cudaGetLastError();
+            h->prefetch = VMT_PREFETCH_OFF;
+            prefetch_now = false;
+        }
+    }
     fn<<<(unsigned)grid, v.NT, smem, st>>>(p);
     VMT_CUDA(cudaGetLastError());
     h->cnt.gen += 1;
@@ -864,7 +883,6 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
         // launched after the generation kernel so its CTAs take the resources
         // the generation CTAs leave free on every SM
         try {
-            h->chunks_alt.reserve((size_t)C * kN * h->L);
             VMT_CUDA(cudaStreamWaitEvent(h->side, h->ev_chunks, 0));
             // a cached matrix for the delta or for a base at most 4 blocks below
             // it (the rest regenerated in place, as in gemm_position)
@@ -899,8 +917,7 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     if (prefetch_now) {
         // launched after the generation kernel so its CTAs take the resources
         // the generation wave leaves free on every SM
-        const std::uint64_t* dp = skip_poly(h, next_b0 - b0);
-        h->chunks_alt.reserve((size_t)C * kN * h->L);
+        const std::uint64_t* dp = pref_dp;
         VMT_CUDA(cudaStreamWaitEvent(h->side, h->ev_chunks, 0));
         AffineJobs a;
         a.n = (int)(C * h->L);
@@ -1046,6 +1063,20 @@ DevBuf<T>& thread_scratch(int device, int slot) {
     return *b;
 }
 DevBuf<std::uint32_t>& thread_scratch_u32(int device, int slot) { return thread_scratch<std::uint32_t>(device, slot); }
+
+// Scratch larger than this is freed when the call that grew it returns (after
+// its final synchronisation), so one large host-destination batch fill does
+// not pin gigabytes of device memory outside the caller's allocator for the
+// rest of the thread's life; smaller buffers stay cached for reuse.
+constexpr size_t kScratchKeepBytes = 64ull << 20;
+template <class T>
+void trim_scratch(DevBuf<T>& b) {
+    if (b.cap * sizeof(T) > kScratchKeepBytes) {
+        cudaFree(b.p);
+        b.p = nullptr;
+        b.cap = 0;
+    }
+}
 
 void build_dephased(int device, cudaStream_t st, std::uint32_t seed0, unsigned ngen, unsigned L, unsigned q,
                     std::uint32_t* dst, DevBuf<std::uint64_t>& polybuf, Counters& cnt) {
@@ -1421,6 +1452,8 @@ int vmt_batch_fill_u32(uint32_t seed0, unsigned ngen, unsigned lanes, unsigned j
         if (!dev)
             VMT_CUDA(cudaMemcpyAsync(dst, scratch.p, (size_t)ngen * n_per_gen * 4, cudaMemcpyDeviceToHost, st));
         VMT_CUDA(cudaStreamSynchronize(st));
+        trim_scratch(scratch);
+        trim_scratch(states);
     });
 }
 
@@ -1477,6 +1510,7 @@ int vmt_jump_states(const uint32_t* src, uint64_t n, const uint64_t* distances, 
         else
             VMT_CUDA(cudaMemcpyAsync(dst, buf.p, n * kN * 4, cudaMemcpyDeviceToHost, st));
         VMT_CUDA(cudaStreamSynchronize(st));
+        trim_scratch(buf);
     });
 }
 

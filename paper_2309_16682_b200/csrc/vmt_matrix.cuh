@@ -155,71 +155,12 @@ constexpr int kWB = kN * 32; // 19968 word-bit columns
 // effective index e <-> word-bit column: e = 0 <-> 31, e >= 1 <-> e + 31
 __device__ __forceinline__ int wb_to_eff(int c) { return c == 31 ? 0 : (c >= 32 ? c - 31 : -1); }
 
-// mwt[j][i] = 1 when input column i contributes to output column j of F^d,
-// from the 19937 effective rows of F^d (row e_in, bit e_out).
-__global__ void vmt_gemm_matrix_kernel(const std::uint64_t* __restrict__ rows, std::int8_t* __restrict__ mwt) {
-    const int ic = blockIdx.x * blockDim.x + threadIdx.x;
-    const int jc = blockIdx.y;
-    if (ic >= kWB)
-        return;
-    const int i = wb_to_eff(ic), j = wb_to_eff(jc);
-    std::int8_t v = 0;
-    if (i >= 0 && j >= 0)
-        v = (std::int8_t)((rows[(long long)i * kRowWords + (j >> 6)] >> (j & 63)) & 1ull);
-    mwt[(long long)jc * kWB + ic] = v;
-}
-
-// a[r][32k + b] = bit b of word k of state r; states interleaved [c][624][L],
-// r = c*L + t, one thread per state word (coalesced reads, 32-byte writes).
-__global__ void vmt_states_to_i8_kernel(const std::uint32_t* __restrict__ st, int L, long long nwords,
-                                        std::int8_t* __restrict__ a) {
-    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= nwords)
-        return;
-    const int t = (int)(idx % L);
-    const long long ck = idx / L;
-    const int k = (int)(ck % kN);
-    const long long r = (ck / kN) * L + t;
-    std::uint32_t w = st[idx];
-    if (k == 0)
-        w &= kUpperMask;
-    std::uint32_t q[8];
-#pragma unroll
-    for (int n = 0; n < 8; ++n) {
-        const std::uint32_t nib = (w >> (4 * n)) & 15u;
-        q[n] = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
-    }
-    uint4* dst = reinterpret_cast<uint4*>(a + r * kWB + 32 * k);
-    dst[0] = make_uint4(q[0], q[1], q[2], q[3]);
-    dst[1] = make_uint4(q[4], q[5], q[6], q[7]);
-}
-
-// new word k of state r = sum_b (prod[r][32k + b] & 1) << b (word 0: its live bit)
-__global__ void vmt_i32_to_states_kernel(const std::int32_t* __restrict__ prod, int L, long long nwords,
-                                         std::uint32_t* __restrict__ st) {
-    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= nwords)
-        return;
-    const int t = (int)(idx % L);
-    const long long ck = idx / L;
-    const int k = (int)(ck % kN);
-    const long long r = (ck / kN) * L + t;
-    const int4* src = reinterpret_cast<const int4*>(prod + r * kWB + 32 * k);
-    std::uint32_t w = 0;
-#pragma unroll
-    for (int n = 0; n < 8; ++n) {
-        const int4 v = src[n];
-        w |= ((std::uint32_t)v.x & 1u) << (4 * n) | ((std::uint32_t)v.y & 1u) << (4 * n + 1) |
-             ((std::uint32_t)v.z & 1u) << (4 * n + 2) | ((std::uint32_t)v.w & 1u) << (4 * n + 3);
-    }
-    st[idx] = k == 0 ? (w & kUpperMask) : w;
-}
-
 } // namespace vmt_b200
 
-// FP4 (e2m1) variants of the GEMM positioning operands: 1.0 = code 0x2, two
+// FP4 (e2m1) GEMM positioning operands (vmt_posmma.cuh): 1.0 = code 0x2, two
 // values per byte, low nibble first; unit block scales make the product exact
-// (0/1 inputs, fp32 accumulation of at most 19937 ones).
+// (0/1 inputs, fp32 accumulation of at most 19937 ones). The tcgen05 kernel's
+// epilogue packs the parities of the accumulators straight back into words.
 namespace vmt_b200 {
 
 __global__ void vmt_gemm_matrix_fp4_kernel(const std::uint64_t* __restrict__ rows, std::uint8_t* __restrict__ mwt) {
@@ -266,28 +207,6 @@ __global__ void vmt_states_to_fp4_kernel(const std::uint32_t* __restrict__ st, i
         q[m] = v;
     }
     *reinterpret_cast<uint4*>(a + r * (kWB / 2) + 16 * k) = make_uint4(q[0], q[1], q[2], q[3]);
-}
-
-// inverse: row r = c*nl + j of the fp32 product -> lane lane0+j of state c
-__global__ void vmt_f32_to_states_kernel(const float* __restrict__ prod, int L, int lane0, int nl, long long nwords,
-                                         std::uint32_t* __restrict__ st) {
-    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= nwords)
-        return;
-    const int j = (int)(idx % nl);
-    const long long ck = idx / nl;
-    const int k = (int)(ck % kN);
-    const long long c = ck / kN;
-    const long long r = c * nl + j;
-    const float4* src = reinterpret_cast<const float4*>(prod + r * kWB + 32 * k);
-    std::uint32_t w = 0;
-#pragma unroll
-    for (int n = 0; n < 8; ++n) {
-        const float4 v = src[n];
-        w |= ((std::uint32_t)(int)v.x & 1u) << (4 * n) | ((std::uint32_t)(int)v.y & 1u) << (4 * n + 1) |
-             ((std::uint32_t)(int)v.z & 1u) << (4 * n + 2) | ((std::uint32_t)(int)v.w & 1u) << (4 * n + 3);
-    }
-    st[(c * kN + k) * L + lane0 + j] = k == 0 ? (w & kUpperMask) : w;
 }
 
 } // namespace vmt_b200

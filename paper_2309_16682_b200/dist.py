@@ -31,20 +31,33 @@ def fold_xor(parts: Sequence[int]) -> int:
     return x
 
 
-def combine_xor(partial: int, device: torch.device | str = "cpu") -> int:
+def collective_device(device: torch.device | str | None = None) -> torch.device:
+    """Where the collectives' tensors live: the caller's choice, else this
+    rank's current CUDA device under NCCL (which only moves device memory),
+    else the CPU (gloo)."""
+    if device is not None:
+        return torch.device(device)
+    if dist.is_initialized() and dist.get_backend() == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def combine_xor(partial: int, device: torch.device | str | None = None) -> int:
     """XOR of every rank's 32-bit partial (all-gather + local fold)."""
     if not dist.is_initialized() or dist.get_world_size() == 1:
         return partial & 0xFFFFFFFF
     world = dist.get_world_size()
+    device = collective_device(device)
     t = torch.tensor([partial & 0xFFFFFFFF], dtype=torch.int64, device=device)
     out = [torch.zeros_like(t) for _ in range(world)]
     dist.all_gather(out, t)
     return fold_xor(int(o.item()) for o in out)
 
 
-def max_over_ranks(value: float, device: torch.device | str = "cpu") -> float:
+def max_over_ranks(value: float, device: torch.device | str | None = None) -> float:
     if not dist.is_initialized() or dist.get_world_size() == 1:
         return value
+    device = collective_device(device)
     t = torch.tensor([value], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())

@@ -9,6 +9,9 @@
   posmma: vmt_posmma2_kernel, the co-resident tcgen05 FP4 positioning GEMM (CTA pairs)
           (4736 lane states x F^(624 D)); under ncu it runs serialised, i.e.
           alone on the GPU (6 fills of 2^32 words; it launches from fill 3 on)
+  c1/c2/c3: the other BASELINE configs as bench.py's extras run them (8
+          repeats of each call, past the one-time matrix builds) -- for the
+          launch lists showing every kernel is ours
 Each target runs its call three times; profile with --launch-skip/-c on the
 kernel name (see profiles/scripts/profile.sh).
 """
@@ -21,6 +24,27 @@ import paper_2309_16682_b200 as V  # noqa: E402
 
 what = sys.argv[1]
 n = 1 << 32
+if what in ("c1", "c2", "c3"):
+    if what == "c1":
+        g = V.VmtGenerator(5489, V.VmtConfig(16))
+        b = torch.empty(1 << 26, dtype=torch.uint32, device="cuda")
+        for _ in range(8):
+            g.fill_u32(b)
+    elif what == "c2":
+        g = V.VmtGenerator(42, V.VmtConfig(8))
+        f = torch.empty(1 << 28, dtype=torch.float32, device="cuda")
+        d = torch.empty(1 << 28, dtype=torch.float64, device="cuda")
+        for _ in range(8):
+            g.fill_f32(f)
+        for _ in range(8):
+            g.fill_f64(d)
+    else:
+        b = torch.empty(1024 << 20, dtype=torch.uint32, device="cuda")
+        for _ in range(4):
+            V.batch_fill_u32(b, 1, 1024, 16, 1 << 20)
+    torch.cuda.synchronize()
+    print("done", what)
+    sys.exit(0)
 g = V.VmtGenerator(5489, V.VmtConfig(32))
 g.set_tuning(max_chunks=148)
 if what in ("gen", "jump"):

@@ -39,6 +39,20 @@ def test_library_is_sm100a():
     assert "sm_100a" in out.stdout
 
 
+def test_library_links_no_cuda_math_library():
+    """Every kernel on the path is ours: the library needs no cuBLAS/cuBLASLt
+    (or any other CUDA library; the runtime is linked statically)."""
+    import subprocess
+    import paper_2309_16682_b200._capi as capi
+    out = subprocess.run(["readelf", "-d", capi.LIB_PATH], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("readelf unavailable")
+    needed = [ln.split("[")[1].rstrip("]") for ln in out.stdout.splitlines() if "(NEEDED)" in ln]
+    assert needed, out.stdout
+    for lib in needed:
+        assert not any(x in lib for x in ("cublas", "cudnn", "cufft", "curand", "cusparse", "libcudart")), needed
+
+
 def test_full_period_exponents():
     import paper_2309_16682_b200 as V
     # jump.cpp:13-15, test_jump.cpp:32-38 (+ L=32)
@@ -133,3 +147,22 @@ def test_argument_errors_without_gpu():
     with pytest.raises(V.InvalidArgument):
         V.write_jump_matrix_file("/tmp/never.vmtj", np.zeros(5, np.uint64), 1)
     assert b"invalid" in lib.vmt_status_string(_capi.VMT_EINVAL)
+
+
+@pytest.mark.parametrize("fill,dt", [("fill_u32", "uint32"), ("fill_f32", "float32"), ("fill_f64", "float64")])
+def test_fill_rejects_n_beyond_buffer(fill, dt):
+    """Every fill checks n against the destination's size before calling the
+    C ABI (which cannot see the buffer's extent)."""
+    import numpy as np
+    import paper_2309_16682_b200 as V
+    g = V.VmtGenerator.__new__(V.VmtGenerator)  # no device needed: the check comes first
+    g._h = None
+    with pytest.raises(V.InvalidArgument):
+        getattr(g, fill)(np.empty(8, dt), n=9)
+
+
+def test_dist_collective_device_defaults():
+    import torch
+    from paper_2309_16682_b200 import dist as D
+    assert D.collective_device() == torch.device("cpu")  # no process group: CPU
+    assert D.collective_device("cuda:3") == torch.device("cuda", 3)

@@ -68,9 +68,33 @@ def test_gemm_positioning_mode2_and_shape_changes():
     assert gem.positioning_stats()["gemm_positionings"] >= 2
 
 
-def test_int8_backend_matches():
-    """The int8 GEMM backend (used where cuBLASLt has no FP4 kernel; forced
-    here by VMT_GEMM_INT8) gives the same words."""
+@pytest.mark.parametrize("L,chunks", [(16, 75), (16, 65), (8, 130)])
+def test_small_row_counts_on_own_kernel(L, chunks):
+    """Below 2048 lane states (config 1's 75 chunks x 16 lanes = 1200 rows,
+    row counts that are not a multiple of the 256-row CTA-pair tile) the
+    positioning GEMM is our tcgen05 kernel too (no cuBLAS in the library):
+    same words as the polynomial jumps."""
+    n = (1 << 25) + 7
+    ref = V.VmtGenerator(21, V.VmtConfig(L))
+    gem = V.VmtGenerator(21, V.VmtConfig(L))
+    for g in (ref, gem):
+        g.set_tuning(max_chunks=chunks)
+    ref.set_positioning(1)
+    gem.set_positioning(2)
+    gem.set_prefetch(0)
+    a = torch.empty(n, dtype=torch.uint32, device="cuda")
+    b = torch.empty(n, dtype=torch.uint32, device="cuda")
+    for i in range(4):
+        ref.fill_u32(a)
+        gem.fill_u32(b)
+        torch.cuda.synchronize()
+        assert torch.equal(i32(a), i32(b)), i
+    assert gem.positioning_stats()["gemm_positionings"] >= 2
+
+
+def test_single_cta_kernel_matches():
+    """The single-CTA tcgen05 form (VMT_POSMMA_SINGLE, M=128 tiles) gives the
+    same words as the polynomial jumps."""
     import os
     import subprocess
     import sys
@@ -91,7 +115,7 @@ print("ok")
 '''
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
-                       env=dict(os.environ, VMT_GEMM_INT8="1"))
+                       env=dict(os.environ, VMT_POSMMA_SINGLE="1"))
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
