@@ -103,9 +103,27 @@ __device__ __forceinline__ std::uint32_t mad_lo(std::uint32_t a, std::uint32_t b
     asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
     return r;
 }
+// Right shifts by s as the high word of a multiply by 2^(32-s) (IMAD.HI, FMA
+// pipe) instead of SHF (ALU pipe): the twist + temper is ALU-pipe bound, so
+// moving some of the three right shifts per word to the FMA pipe balances the
+// two pipes. Bit 0: the twist's u >> 1; bit 1: temper's y >> 11; bit 2:
+// temper's y >> 18.
+#ifndef VMT_SHR_FMA
+#define VMT_SHR_FMA 0
+#endif
+template <int S, bool FMA>
+__device__ __forceinline__ std::uint32_t shr(std::uint32_t x) {
+    if (FMA) {
+        std::uint32_t r;
+        asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "n"(1u << (32 - S)));
+        return r;
+    }
+    return x >> S;
+}
+
 __device__ __forceinline__ std::uint32_t twist(std::uint32_t xk, std::uint32_t xk1, std::uint32_t xm) {
     const std::uint32_t u = lop3_sel_hi(xk, xk1);
-    const std::uint32_t uh = u >> 1;
+    const std::uint32_t uh = shr<1, (VMT_SHR_FMA & 1) != 0>(u);
 #if VMT_TWIST_FMA_MAG
     // mag = (u & 1) * A = u*A - (u >> 1)*2A: two IMADs on the FMA pipe instead
     // of a LOP3 + IMAD, so the twist costs 3 ALU-pipe ops (LOP3, SHF, LOP3)
@@ -120,10 +138,10 @@ __device__ __forceinline__ std::uint32_t twist(std::uint32_t xk, std::uint32_t x
 // are multiplies so they issue on the FMA pipe. (Right shifts as the high word
 // of IMAD.WIDE were measured 6% slower: the wide multiply is not FMA-pipe only.)
 __device__ __forceinline__ std::uint32_t temper(std::uint32_t y) {
-    y ^= y >> 11;
+    y ^= shr<11, (VMT_SHR_FMA & 2) != 0>(y);
     y = xor_and<0x9D2C5680u>(y, mul_lo(y, 1u << 7));
     y = xor_and<0xEFC60000u>(y, mul_lo(y, 1u << 15));
-    return y ^ (y >> 18);
+    return y ^ shr<18, (VMT_SHR_FMA & 4) != 0>(y);
 }
 
 template <int V>
