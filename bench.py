@@ -108,8 +108,17 @@ class ClockSampler:
         get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
             nv.nvmlDeviceGetCurrentClocksThrottleReasons
         mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        i = 0
         while True:
-            self.rows.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)), float(mx), int(get_reasons(h))))
+            watts = None
+            if i % 8 == 0:  # (the power query is slower than the clock queries)
+                try:
+                    watts = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                except Exception:
+                    pass
+            i += 1
+            self.rows.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)), float(mx), int(get_reasons(h)),
+                              watts))
             if self.stop_flag.wait(0.005):
                 break
 
@@ -141,7 +150,11 @@ class ClockSampler:
             for i, nm in enumerate(names):
                 if r[4 + i].lower() == "active":
                     bits |= self.BITS[nm]
-            self.rows.append((float(r[0]), float(r[1]) if r[1].replace(".", "").isdigit() else 0.0, bits))
+            try:
+                watts = float(r[2])
+            except ValueError:
+                watts = None
+            self.rows.append((float(r[0]), float(r[1]) if r[1].replace(".", "").isdigit() else 0.0, bits, watts))
 
     def stop(self) -> dict:
         if self.src is None:
@@ -157,10 +170,13 @@ class ClockSampler:
             self.stop_flag.set()
             self.thread.join(timeout=2)
         rows = list(self.rows)
-        reasons = sorted({nm for _, _, bits in rows for nm, b in self.BITS.items() if bits & b})
+        reasons = sorted({nm for _, _, bits, _ in rows for nm, b in self.BITS.items() if bits & b})
+        watts = [r[3] for r in rows if r[3] is not None]
         return {"sm_mhz": statistics.median(r[0] for r in rows) if rows else None,
                 "sm_max_mhz": max(r[1] for r in rows) if rows else None,
                 "sm_min_mhz": min(r[0] for r in rows) if rows else None,
+                "power_w_median": statistics.median(watts) if watts else None,
+                "power_w_max": max(watts) if watts else None,
                 "reasons": reasons, "samples": len(rows), "source": self.src}
 
 
@@ -217,6 +233,34 @@ def reference_cpu(words: int, threads: int, q: int = 16):
     return per * threads / secs, secs, x, per * threads
 
 
+# how oracle/_ref/libvmtref.so is compiled (oracle/Makefile REF_FLAGS): the
+# paper's AVX-512 flags, not -march=native -- the library is built in the
+# build container and must run on whichever host the GPU box has
+REF_BUILD_FLAGS = "g++ -std=c++20 -O3 -mavx2 -mavx512f -mavx512dq"
+
+
+def reference_simd() -> dict:
+    """SIMD width of the reference's lane backends on this host
+    (has_simd_lanes<N>, lane_ops.hpp:227-230) and the build flags."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import RefLib
+    ref = RefLib()
+    lanes = {n: bool(ref.lib.vref_simd_backend(n)) for n in (4, 8, 16)}
+    width = max([n * 32 for n, ok in lanes.items() if ok], default=32)
+    flags = set()
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("flags"):
+                    flags = set(line.split(":", 1)[1].split())
+                    break
+    except Exception:
+        pass
+    isa = "AVX-512" if "avx512f" in flags else ("AVX2" if "avx2" in flags else "SSE2")
+    return {"simd_bits": width, "engine": "VmtEngine<16>", "lane_backends": {str(k): v for k, v in lanes.items()},
+            "host_isa": isa, "build": REF_BUILD_FLAGS}
+
+
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -255,29 +299,73 @@ def extras(dev) -> dict:
         return e0.elapsed_time(e1) / reps * 1e-3
 
     out = {}
+    peak = measured_peak()[0]
+
+    def hbm(nbytes, secs):
+        gbs = nbytes / secs / 1e9
+        return {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak}
+
+    def fill_breakdown(g, fn, reps=3):
+        # per-fill generation-kernel time and the wait for the positioning
+        # (CUDA events around both, vmt_profile_totals)
+        g.set_profiling(True)
+        g.profile_totals()
+        for _ in range(reps):
+            fn()
+        torch.cuda.synchronize(dev)
+        f, j, gm = g.profile_totals()
+        g.set_profiling(False)
+        return {"gen_kernel_ms": gm / max(f, 1), "positioning_wait_ms": j / max(f, 1)}
+
+    def stated(roof, bd, what_gen, what_pos):
+        # the bound is the larger of the generation kernel and the positioning
+        # wait (the next fill's chunk states, computed by the co-resident
+        # tcgen05 GEMM during this fill's generation kernel)
+        pos_bound = bd["positioning_wait_ms"] > 0.25 * bd["gen_kernel_ms"]
+        roof = dict(roof, breakdown_ms=bd, limited_by=what_pos if pos_bound else what_gen)
+        return roof
+
     # c1: L=16, seed 5489, full-period de-phasing, 2^26 uint32 (setup excluded, like bench.hpp:27-30)
     n = 1 << 26
     buf = torch.empty(n, dtype=torch.uint32, device=dev)
     g = V.VmtGenerator(5489, V.VmtConfig(16))
     s = timed(lambda: g.fill_u32(buf))
-    out["c1_L16_2p26_u32"] = {"value": n / s, "unit": "uint32/s", "ms": s * 1e3}
+    bd = fill_breakdown(g, lambda: g.fill_u32(buf))
+    out["c1_L16_2p26_u32"] = {"value": n / s, "unit": "uint32/s", "ms": s * 1e3, "roofline": stated(
+        hbm(n * 4, s), bd, "generation kernel (HBM stores)",
+        "positioning GEMM: every fill re-positions all C x 16 chunk lane states (1200 rows x 19968^2 FP4 MACs, "
+        "~0.23 ms alone, co-resident with the 0.11-0.18 ms generation kernel); see DESIGN.md section 6")}
     # c2: L=8, seed 42, 2^28 -> float32 and float64 in [0,1)
     n = 1 << 28
     f32 = torch.empty(n, dtype=torch.float32, device=dev)
     g = V.VmtGenerator(42, V.VmtConfig(8))
     s = timed(lambda: g.fill_f32(f32))
-    out["c2_L8_2p28_f32"] = {"value": n / s, "unit": "float32/s", "ms": s * 1e3, "gbs": n * 4 / s / 1e9}
+    bd = fill_breakdown(g, lambda: g.fill_f32(f32))
+    out["c2_L8_2p28_f32"] = {"value": n / s, "unit": "float32/s", "ms": s * 1e3, "gbs": n * 4 / s / 1e9,
+                             "roofline": stated(hbm(n * 4, s), bd, "generation kernel (HBM stores)",
+                                                "positioning GEMM (296 chunks x 8 lanes = 2368 rows per fill)")}
     del f32
     f64 = torch.empty(n, dtype=torch.float64, device=dev)
     s = timed(lambda: g.fill_f64(f64))
-    out["c2_L8_2p28_f64"] = {"value": n / s, "unit": "float64/s", "ms": s * 1e3, "gbs": n * 8 / s / 1e9}
+    bd = fill_breakdown(g, lambda: g.fill_f64(f64))
+    out["c2_L8_2p28_f64"] = {"value": n / s, "unit": "float64/s", "ms": s * 1e3, "gbs": n * 8 / s / 1e9,
+                             "roofline": stated(hbm(n * 8, s), bd,
+                                                "generation kernel: 8-byte elements, one double per word "
+                                                "(I2F.F64 + DMUL per word, 148 chunks)",
+                                                "positioning GEMM (148 chunks x 8 lanes = 1184 rows per fill)")}
     del f64
     # c3: 1024 generators (L=16, seeds 1..1024, full period) x 2^20 words, generator-major,
     # including the 1024 x 15 de-phasing jumps
     n = 1 << 20
     b3 = torch.empty(1024 * n, dtype=torch.uint32, device=dev)
     s = timed(lambda: V.batch_fill_u32(b3, 1, 1024, 16, n), reps=2)
-    out["c3_1024xL16_2p20_u32"] = {"value": 1024 * n / s, "unit": "uint32/s", "ms": s * 1e3,
+    # the same call without generation (n_per_gen = 0: seeding + de-phasing only)
+    tc = timed(lambda: V.batch_fill_u32(b3, 1, 1024, 16, 0), reps=2)
+    r3 = hbm(1024 * n * 4, s)
+    r3.update(breakdown_ms={"seed_and_dephase": tc * 1e3, "generation": (s - tc) * 1e3},
+              limited_by="de-phasing: log2(16) = 4 FP4 tcgen05 GEMMs over 1024 x (1+2+4+8) lane states "
+                         "(15360 rows x 19968^2 MACs) before 4 GiB of generation")
+    out["c3_1024xL16_2p20_u32"] = {"value": 1024 * n / s, "unit": "uint32/s", "ms": s * 1e3, "roofline": r3,
                                    "note": "includes seeding + de-phasing of 15360 lane states (four FP4 GEMMs, matrices cached)"}
     del b3
     # c5: 4096 states (seeds 1..4096) jumped by 64-bit distances, then 624 outputs each
@@ -287,16 +375,24 @@ def extras(dev) -> dict:
     jumped = torch.empty_like(states)
     s = timed(lambda: V.jump_states(states, dists, out=jumped), reps=2)
     out["c5_4096_jumps_64bit"] = {"value": 4096 / s, "unit": "state jumps/s", "ms": s * 1e3,
+                                  "roofline": {"bound": "alu", "limited_by": "integer ALU issue of the polynomial "
+                                               "jump (p(F)s as a word convolution: ~19960 coefficient steps x 20 "
+                                               "words x LOP3 per jump); see profiles/r02_summary.md"},
                                   "note": "4 polynomial jumps per state from 12-bit digit tables (bits 16..63 of the 64-bit distance) + a direct advance by the low 16 bits"}
     # fused statistics consumer (monobit + chi2 byte histogram), 2^32 words, nothing stored
     n = 1 << 32
     g = V.VmtGenerator(5489, V.VmtConfig(32))
     s = timed(lambda: g.stat_counts(n), reps=2)
-    out["stats_consumer_L32_2p32"] = {"value": n / s, "unit": "uint32/s", "ms": s * 1e3}
+    out["stats_consumer_L32_2p32"] = {"value": n / s, "unit": "uint32/s", "ms": s * 1e3,
+                                      "roofline": {"bound": "smem-atomic", "limited_by": "4 shared-memory atomics "
+                                                   "per tempered word (byte histogram), ~0.31 warp-ATOMS per clock "
+                                                   "per SM; nothing stored (DESIGN.md section 4.5)"}}
     # full-period jump matrix F^(2^19932) (the reference needs ~50 h of squarings)
     rows = torch.empty((19937, 312), dtype=torch.uint64, device=dev)
     s = timed(lambda: V.jump_matrix_pow2(19932, out=rows), reps=2)
-    out["jump_matrix_2p19932"] = {"value": s * 1e3, "unit": "ms", "note": "19937 basis-state polynomial jumps"}
+    out["jump_matrix_2p19932"] = {"value": s * 1e3, "unit": "ms", "note": "19937 basis-state polynomial jumps",
+                                  "roofline": {"bound": "alu", "limited_by": "the polynomial jump kernel "
+                                               "(19937 jobs), as c5"}}
     return out
 
 
@@ -324,7 +420,7 @@ def run_reference(args):
                            "(throughput is independent of q; full-period matrices take ~50 h)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                          "sample": f"{words} uint32 per step, {threads} threads x VmtEngine<16>::next_block_state "
-                                   f"into DRAM ({cpu_model()})"},
+                                   f"into DRAM ({cpu_model()})", "simd": reference_simd()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -358,6 +454,9 @@ def main():
         if shared:
             dist.init_process_group("gloo")
         else:
+            # communicator / nranks lines on stderr (the JSON line is on stdout)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
     coll = torch.device("cpu") if shared else dev  # device of the collectives' tensors
     # T = words the whole job generates per step (all ranks)
@@ -457,7 +556,10 @@ def main():
         g.skip(T - count)
     xs = max_over_ranks((time.perf_counter() - t0) / args.steps, coll)
     e2e_xor = {"value": T / xs, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 4 * world,
-               "ms_per_step": xs * 1e3, "mode": "fused XOR checksum, nothing stored"}
+               "ms_per_step": xs * 1e3, "mode": "fused XOR checksum, nothing stored",
+               "note": "temper-free algebraic path: the kernel XORs the untempered words and tempers the "
+                       "fold once (temper is GF(2)-linear) -- valid for this consumer only; the general "
+                       "fused consumer that tempers every word is other_configs.stats_consumer_L32_2p32"}
 
     # -- end to end into pinned host memory through the public API
     e2e = None
@@ -467,8 +569,18 @@ def main():
     # the full 64 GiB share, so 8 ranks pin 128 GiB rather than 512 GiB; the
     # number is PCIe-bound and does not depend on the size past a few GiB)
     ew = count if world == 1 else min(count, 1 << 32)
+    # never pin more than half of the host's available memory across the
+    # node's ranks (one node: every rank of the job shares this host)
+    try:
+        import psutil
+        avail_words = psutil.virtual_memory().available // 2 // world // 4
+        ew = min(ew, max(avail_words >> 24 << 24, 0))
+    except Exception:
+        pass
     Te = ew * world
-    if not args.no_e2e and args.mode == "store":
+    if not args.no_e2e and args.mode == "store" and ew < (1 << 26):
+        e2e = {"unavailable": f"host memory too small for a pinned end-to-end buffer per rank ({ew} words)"}
+    elif not args.no_e2e and args.mode == "store":
         host, kind = None, None
         try:
             host = torch.empty(ew, dtype=torch.uint32, pin_memory=True)
@@ -524,6 +636,17 @@ def main():
             del src
         del host
 
+    # every rank's own step time, clocks and throughput (rank 0 prints them)
+    mine = {"rank": rank, "device": local, "ms_per_step_local": e0.elapsed_time(e1) / args.steps,
+            "gen_kernel_ms": gen_tot / max(fills, 1), "per_gpu_value": count / (e0.elapsed_time(e1) / args.steps * 1e-3),
+            "sm_mhz": clk.get("sm_mhz") if isinstance(clk, dict) else None,
+            "reasons": clk.get("reasons") if isinstance(clk, dict) else None}
+    if world > 1:
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, mine)
+    else:
+        per_rank = [mine]
+
     peak, peak_src = measured_peak()
     # second denominator: pure-store probes over the same 64 GiB (after the
     # bench's own buffers are released)
@@ -548,6 +671,7 @@ def main():
                    "parallelism": f"stream partition x{world} ({args.scaling})"},
         "gpu_launches": launches,
         "per_gpu_value": count / (ms * 1e-3),
+        "per_rank": per_rank,
         "timing_breakdown_ms": {"gen_kernel": gen_ms, "positioning": jump_ms, "setup_create": setup_ms,
                                 "positioning_gemms": g.positioning_stats()["gemm_positionings"],
                                 "prefetch": g.prefetch_stats(),
@@ -577,7 +701,8 @@ def main():
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
                                     "sample": f"{done} uint32 (2^32), {threads} threads x VmtEngine<16> "
                                               f"next_block_state into DRAM, q=16 ({cpu_model()}); "
-                                              "L=32 unsupported by the reference"}
+                                              "L=32 unsupported by the reference",
+                                    "simd": reference_simd()}
         except Exception as e:  # the reference build is optional on the box
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {e}"}

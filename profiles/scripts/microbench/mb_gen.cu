@@ -18,13 +18,16 @@ using namespace vmt_b200;
 #ifndef MB_W
 #define MB_W 208
 #endif
+#ifndef MB_L
+#define MB_L 32
+#endif
 #ifndef MB_TMA
 #define MB_TMA false
 #endif
 template <int MODE>
 float run(GenParams p, int grid, int reps, cudaStream_t st) {
-    using S = GenShape<32, MB_R, MB_VW, MB_W, MB_TMA>;
-    auto fn = vmt_gen_kernel<32, 32, MB_R, MB_VW, MB_W, MB_TMA, MODE, true>;
+    using S = GenShape<MB_L, MB_R, MB_VW, MB_W, MB_TMA>;
+    auto fn = vmt_gen_kernel<MB_L, MB_L, MB_R, MB_VW, MB_W, MB_TMA, MODE, true>;
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, S::smem<MODE>()));
     for (int i = 0; i < 3; ++i) fn<<<grid, S::NT, S::smem<MODE>(), st>>>(p);
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
@@ -38,8 +41,8 @@ float run(GenParams p, int grid, int reps, cudaStream_t st) {
 
 int main(int argc, char** argv) {
     const int reps = argc > 1 ? atoi(argv[1]) : 20;
-    const int C = argc > 2 ? atoi(argv[2]) : 148, L = 32;
-    const unsigned long long B = 1453ull * 148 / C; // blocks per chunk: 148 * 1453 * 19968 ~ 2^32 words
+    const int C = argc > 2 ? atoi(argv[2]) : 148, L = MB_L;
+    const unsigned long long B = argc > 3 ? strtoull(argv[3], nullptr, 10) : 1453ull * 148 / C * 32 / L; // blocks per chunk: 148 * 1453 * 19968 ~ 2^32 words
     const unsigned long long n = (unsigned long long)C * B * kN * L;
     std::vector<unsigned> h((size_t)C * kN * L);
     unsigned s = 12345;
@@ -60,10 +63,10 @@ int main(int argc, char** argv) {
     CK(cudaMemcpy(hp.data(), parts, C * 4, cudaMemcpyDeviceToHost));
     unsigned x = 0; for (auto v : hp) x ^= v;
     // XOR of a sample of the stored output (first/last MB)
-    std::vector<unsigned> ho(1 << 18);
+    std::vector<unsigned> ho(std::min<unsigned long long>(1 << 18, n));
     CK(cudaMemcpy(ho.data(), out + n - ho.size(), ho.size() * 4, cudaMemcpyDeviceToHost));
     unsigned y = 0; for (auto v : ho) y ^= v;
-    printf("{\"tma\": %d, \"R\": %d, \"W\": %d, \"C\": %d, \"vw\": %d, \"shr_fma\": %d, \"store_ms\": %.4f, \"store_tbs\": %.4f, \"temperxor_ms\": %.4f, \"temperxor_words_s\": %.4e, \"chk\": \"%08x-%08x\"}\n",
-           (int)MB_TMA, MB_R, MB_W, C, MB_VW, VMT_SHR_FMA, ms_store, n * 4.0 / ms_store / 1e9, ms_xor, n / (ms_xor * 1e-3), x, y);
+    printf("{\"L\": %d, \"tma\": %d, \"R\": %d, \"W\": %d, \"C\": %d, \"vw\": %d, \"shr_fma\": %d, \"store_ms\": %.4f, \"store_tbs\": %.4f, \"words_s_per_chunk\": %.4e, \"temperxor_ms\": %.4f, \"temperxor_words_s\": %.4e, \"chk\": \"%08x-%08x\"}\n",
+           MB_L, (int)MB_TMA, MB_R, MB_W, C, MB_VW, VMT_SHR_FMA, ms_store, n * 4.0 / ms_store / 1e9, n / (ms_store * 1e-3) / C, ms_xor, n / (ms_xor * 1e-3), x, y);
     return 0;
 }

@@ -74,13 +74,17 @@ def test_multi_gpu_fill_partition_and_checksum():
     ref = torch.empty(n, dtype=torch.uint32, device="cuda")
     V.VmtGenerator(5489, V.VmtConfig(32)).fill_u32(ref)
     x_ref = V.VmtGenerator(5489, V.VmtConfig(32)).checksum_xor(n)
-    # three "devices" (all device 0 on a one-GPU box): same partition logic
-    devs = [0, 0, 0]
+    # three parts on distinct devices when the box has them (round robin over
+    # the visible GPUs; all on device 0 on a one-GPU box: same partition logic)
+    ndev = torch.cuda.device_count()
+    devs = [k % ndev for k in range(3)]
     sizes = [n // 3 + (1 if k < n % 3 else 0) for k in range(3)]
-    outs = [torch.empty(s, dtype=torch.uint32, device="cuda") for s in sizes]
+    outs = [torch.empty(s, dtype=torch.uint32, device=f"cuda:{d}") for s, d in zip(sizes, devs)]
     x = V.multi_gpu_fill(5489, 32, n, devs, outs)
     torch.cuda.synchronize()
-    assert torch.equal(torch.cat(outs), ref)
+    for d in set(devs):
+        torch.cuda.synchronize(d)
+    assert torch.equal(torch.cat([o.to(ref.device) for o in outs]), ref)
     assert x == x_ref
     assert V.multi_gpu_fill(5489, 32, n, devs, None) == x_ref  # fused XOR mode
 
