@@ -36,12 +36,17 @@ def _fingerprint() -> str:
             h.update(fh.read())
     with open(os.path.join(ROOT, "include", "vmt19937_b200.h"), "rb") as fh:
         h.update(fh.read())
-    h.update(" ".join(ARCH).encode())
+    h.update(" ".join(ARCH + _extra()).encode())
     return h.hexdigest()
 
 
+def _extra() -> list[str]:
+    """Extra nvcc flags from $VMT_EXTRA_NVCC (experiments, e.g. -DVMT_JUMP_MINB=28)."""
+    return os.environ.get("VMT_EXTRA_NVCC", "").split()
+
+
 def _compile_cmds(objdir: str) -> list[tuple[list[str], str]]:
-    common = [_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-c"]
+    common = [_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", *_extra(), "-c"]
     out = []
     for src in SOURCES:
         obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")

@@ -13,7 +13,7 @@
 // next fill (VMT_PREFETCH_TENSOR). Where the kernel cannot be set up (no TMA
 // descriptor encoder) the caller falls back to the polynomial jumps.
 // The 200 MB FP4 matrix for a delta is built once (19937 basis jumps +
-// expansion) when the delta repeats; two are cached, and deltas up to 4 blocks
+// expansion) when the delta repeats; four are cached, and deltas up to 4 blocks
 // above a cached one reuse it (the rest regenerated in place).
 #include <cudaTypedefs.h>
 
@@ -31,6 +31,10 @@ inline std::uint64_t gemm_min_rows() {
     return v;
 }
 constexpr std::size_t kGemmMatBytes = (std::size_t)kWB * kWB;
+// positioning matrices cached per generator (200 MB each): a generator that
+// alternates between fill shapes (e.g. float and double fills of the same
+// count, each with block deltas D and D+1) keeps all of them
+constexpr std::size_t kGemmCachedMats = 4;
 
 struct GemmPos {
     std::map<std::uint64_t, std::unique_ptr<DevBuf<std::int8_t>>> mats; // delta -> F^(624 delta), FP4 word-bit
@@ -80,24 +84,41 @@ bool posmma_pair() {
     return pair;
 }
 
+// Operand-ring depths the CTA-pair kernel is instantiated for; a launch takes
+// the deepest that fits the shared memory it may use (kP2MaxStages when it
+// runs alone, fewer beside a generation CTA).
+constexpr int kP2MaxStages = 10;
+int p2_stages_for(int smem_bytes) {
+    for (int s : {10, 8, 7, 6, 5, 4})
+        if (p2_smem(s) <= smem_bytes)
+            return s;
+    return 0;
+}
+
 bool posmma_run(GemmPos& gp, const CUtensorMap& tmap_b, const std::uint32_t* src, std::uint32_t* dst, unsigned L,
-                std::uint64_t rows, int sms, cudaStream_t st, unsigned nl, unsigned lane0);
+                std::uint64_t rows, int sms, cudaStream_t st, unsigned nl, unsigned lane0,
+                int stages = kP2MaxStages);
 
 bool posmma_launch(GemmPos& gp, std::uint64_t delta, const std::uint32_t* src, std::uint32_t* dst, unsigned L,
-                   std::uint64_t rows, int sms, cudaStream_t st) {
+                   std::uint64_t rows, int sms, cudaStream_t st, int stages = kP2MaxStages) {
     const bool pair = posmma_pair();
     auto it = (pair ? gp.tmaps2 : gp.tmaps).find(delta);
     if (it == (pair ? gp.tmaps2 : gp.tmaps).end() || !gp.mats.count(delta))
         return false;
     gp.last_use[delta] = gp.tick;
-    return posmma_run(gp, it->second, src, dst, L, rows, sms, st, L, 0);
+    return posmma_run(gp, it->second, src, dst, L, rows, sms, st, L, 0, stages);
+}
+
+template <int S>
+void p2_launch(int grid, cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const PosMmaParams& pp) {
+    vmt_posmma2_kernel<S><<<grid, kPmThreads, p2_smem(S), st>>>(a, b, pp);
 }
 
 // Lanes [lane0, lane0 + nl) of every state of dst (interleaved [.][624][L])
 // = lanes [0, nl) of src times the FP4 matrix behind tmap_b (nl = L, lane0 =
 // 0: every lane, chunk positioning).
 bool posmma_run(GemmPos& gp, const CUtensorMap& tmap_b, const std::uint32_t* src, std::uint32_t* dst, unsigned L,
-                std::uint64_t rows, int sms, cudaStream_t st, unsigned nl, unsigned lane0) {
+                std::uint64_t rows, int sms, cudaStream_t st, unsigned nl, unsigned lane0, int stages) {
     const bool pair = posmma_pair();
     {
         // function attributes are per device (vmt_multi_gpu_fill drives several)
@@ -108,8 +129,18 @@ bool posmma_run(GemmPos& gp, const CUtensorMap& tmap_b, const std::uint32_t* src
         std::lock_guard<std::mutex> lk(mu);
         if (!done.count(dev)) {
             VMT_CUDA(cudaFuncSetAttribute(vmt_posmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPmSmem));
-            VMT_CUDA(
-                cudaFuncSetAttribute(vmt_posmma2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2Smem));
+            VMT_CUDA(cudaFuncSetAttribute(vmt_posmma2_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          p2_smem(4)));
+            VMT_CUDA(cudaFuncSetAttribute(vmt_posmma2_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          p2_smem(5)));
+            VMT_CUDA(cudaFuncSetAttribute(vmt_posmma2_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          p2_smem(6)));
+            VMT_CUDA(cudaFuncSetAttribute(vmt_posmma2_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          p2_smem(7)));
+            VMT_CUDA(cudaFuncSetAttribute(vmt_posmma2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          p2_smem(8)));
+            VMT_CUDA(cudaFuncSetAttribute(vmt_posmma2_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          p2_smem(10)));
             done.insert(dev);
         }
     }
@@ -136,9 +167,17 @@ bool posmma_run(GemmPos& gp, const CUtensorMap& tmap_b, const std::uint32_t* src
     pp.lane0 = (int)lane0;
     pp.m_tiles = (int)(rows_pad / tile_rows);
     const int tiles = pp.m_tiles * kPmNTiles;
-    if (pair)
-        vmt_posmma2_kernel<<<2 * std::min(tiles, sms / 2), kPmThreads, kP2Smem, st>>>(gp.pm_tmap_a, tmap_b, pp);
-    else
+    if (pair) {
+        const int grid = 2 * std::min(tiles, sms / 2);
+        switch (stages >= 10 ? 10 : stages >= 8 ? 8 : stages < 4 ? 4 : stages) {
+        case 10: p2_launch<10>(grid, st, gp.pm_tmap_a, tmap_b, pp); break;
+        case 8: p2_launch<8>(grid, st, gp.pm_tmap_a, tmap_b, pp); break;
+        case 7: p2_launch<7>(grid, st, gp.pm_tmap_a, tmap_b, pp); break;
+        case 6: p2_launch<6>(grid, st, gp.pm_tmap_a, tmap_b, pp); break;
+        case 5: p2_launch<5>(grid, st, gp.pm_tmap_a, tmap_b, pp); break;
+        default: p2_launch<4>(grid, st, gp.pm_tmap_a, tmap_b, pp); break;
+        }
+    } else
         vmt_posmma_kernel<<<std::min(tiles, sms), kPmThreads, kPmSmem, st>>>(gp.pm_tmap_a, tmap_b, pp);
     VMT_CUDA(cudaGetLastError());
     return true;
@@ -158,8 +197,9 @@ void build_gemm_matrix(const Poly& poly, DevBuf<std::int8_t>& m, cudaStream_t st
     VMT_CUDA(cudaStreamSynchronize(st)); // rows is released on return
 }
 
-// The matrix for a delta, building it when there is room: at most two are
-// cached, and one is only replaced after 32 positionings without a use -- so
+// The matrix for a delta, building it when there is room: at most
+// kGemmCachedMats are cached, and one is only replaced after 32 positionings
+// without a use -- so
 // sizes that wander cannot turn every fill into a 10 ms matrix build.
 // nullptr: no matrix (the caller uses the polynomial jumps).
 const std::int8_t* gemm_matrix(vmt_generator* h, GemmPos& gp, std::uint64_t delta, cudaStream_t st) {
@@ -168,7 +208,7 @@ const std::int8_t* gemm_matrix(vmt_generator* h, GemmPos& gp, std::uint64_t delt
         gp.last_use[delta] = gp.tick;
         return it->second->p;
     }
-    if (gp.mats.size() >= 2) {
+    if (gp.mats.size() >= kGemmCachedMats) {
         std::uint64_t victim = 0;
         bool found = false;
         for (auto& kv : gp.mats)

@@ -142,9 +142,14 @@ int prepare_gen(int dev, GenFn fn, int nt, int smem) {
 // Whether one vmt_posmma_kernel CTA fits on an SM beside per_sm CTAs of the
 // generation kernel `fn` (shared memory incl. the 1 KB per-CTA reservation,
 // registers, threads).
-bool posmma_fits(int dev, GenFn fn, int nt, int smem, int per_sm) {
+int p2_stages_for(int smem_bytes);
+
+// Operand-ring depth of the CTA-pair positioning kernel that fits beside
+// per_sm CTAs of the generation kernel `fn` on one SM (shared memory incl. the
+// 1 KB per-CTA reservation, registers, threads); 0 when none does.
+int posmma_fits(int dev, GenFn fn, int nt, int smem, int per_sm) {
     static std::mutex mu;
-    static std::map<std::tuple<int, const void*, int>, bool> memo;
+    static std::map<std::tuple<int, const void*, int>, int> memo;
     std::lock_guard<std::mutex> lk(mu);
     auto key = std::make_tuple(dev, reinterpret_cast<const void*>(fn), per_sm);
     auto it = memo.find(key);
@@ -157,16 +162,18 @@ bool posmma_fits(int dev, GenFn fn, int nt, int smem, int per_sm) {
     // the positioning kernel posmma_run launches: the CTA pair unless VMT_POSMMA_SINGLE
     const bool single = std::getenv("VMT_POSMMA_SINGLE") != nullptr;
     const void* pk = single ? reinterpret_cast<const void*>(vmt_posmma_kernel)
-                            : reinterpret_cast<const void*>(vmt_posmma2_kernel);
-    const int pm_smem = single ? kPmSmem : kP2Smem;
+                            : reinterpret_cast<const void*>(vmt_posmma2_kernel<4>);
     cudaFuncAttributes ga{}, pa{};
     VMT_CUDA(cudaFuncGetAttributes(&ga, reinterpret_cast<const void*>(fn)));
     VMT_CUDA(cudaFuncGetAttributes(&pa, pk));
     auto regs = [](int per_thread, int threads) { // allocation unit: 256 registers per warp
         return ((per_thread * 32 + 255) / 256 * 256) * ((threads + 31) / 32);
     };
-    const bool ok = per_sm * (smem + 1024) + pm_smem + 1024 <= sm_smem &&
-                    per_sm * regs(ga.numRegs, nt) + regs(pa.numRegs, kPmThreads) <= sm_regs &&
+    const int free_smem = sm_smem - per_sm * (smem + 1024) - 1024;
+    int stages = single ? (kPmSmem <= free_smem ? kPmStages : 0) : p2_stages_for(free_smem);
+    if (const char* cap = std::getenv("VMT_PREF_STAGES")) // experiments: cap the co-resident ring depth
+        stages = std::min(stages, std::max(4, std::atoi(cap)));
+    const bool ok = stages > 0 && per_sm * regs(ga.numRegs, nt) + regs(pa.numRegs, kPmThreads) <= sm_regs &&
                     per_sm * nt + kPmThreads <= sm_threads && !std::getenv("VMT_NO_TC_PREFETCH");
     if (ok) {
         // both kernels ask for the full shared-memory carveout: an SM whose
@@ -174,10 +181,15 @@ bool posmma_fits(int dev, GenFn fn, int nt, int smem, int per_sm) {
         // would have no room left for the GEMM CTA
         VMT_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                       cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        VMT_CUDA(cudaFuncSetAttribute(pk, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        for (const void* k : {pk, reinterpret_cast<const void*>(vmt_posmma2_kernel<5>),
+                              reinterpret_cast<const void*>(vmt_posmma2_kernel<6>),
+                              reinterpret_cast<const void*>(vmt_posmma2_kernel<7>),
+                              reinterpret_cast<const void*>(vmt_posmma2_kernel<8>),
+                              reinterpret_cast<const void*>(vmt_posmma2_kernel<10>)})
+            VMT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     }
-    memo[key] = ok;
-    return ok;
+    memo[key] = ok ? stages : 0;
+    return memo[key];
 }
 
 // ------------------------------------------------------- device buffers --
@@ -247,11 +259,12 @@ void powers_parallel(const Poly& J, size_t count, std::vector<Poly>& out, size_t
 
 std::mutex g_poly_mu;
 
-// 12-bit digit tables T_j[v] = x^(v * 2^(16 + 12 j)), j < 4, v < 4096, for
+// 16-bit digit tables T_j[v] = x^(v * 2^(16 + 16 j)), j < 3, v < 65536, for
 // bits 16..63 of a 64-bit jump distance (config 5; the low 16 bits are
-// stepped directly): four jumps per state. 16384 polynomials (40 MB on the
-// device), built once per process by 16 host threads (~0.1 s).
-constexpr int kDigitBits = 12, kDigitBase = 16, kDigits = 4, kDigitVals = 1 << kDigitBits;
+// stepped directly): three jumps per state (four with 12-bit digits: 7.1 ms
+// for config 5's 4096 states). 196608 polynomials (491 MB on the device),
+// built once per process by host threads (~1 s).
+constexpr int kDigitBits = 16, kDigitBase = 16, kDigits = 3, kDigitVals = 1 << kDigitBits;
 struct DigitTables {
     std::vector<Poly> host; // index j*4096 + v (v=0 unused)
     std::map<int, std::unique_ptr<DevBuf<std::uint64_t>>> dev;
@@ -262,7 +275,7 @@ DigitTables& digit_tables() {
     if (t.host.empty()) {
         Gf2Field& F = Gf2Field::instance();
         t.host.assign((size_t)kDigits * kDigitVals, Poly(kPolyWords, 0));
-        constexpr int kParts = 4; // threads per digit position
+        const int kParts = std::max(1u, std::thread::hardware_concurrency()) >= 24 ? 16 : 8; // threads per digit
         std::vector<std::thread> th;
         for (int j = 0; j < kDigits; ++j)
             for (int part = 0; part < kParts; ++part)
@@ -332,11 +345,17 @@ struct Counters {
 void launch_jump_kernel(const JumpParams& jp, cudaStream_t st) {
     int dev = 0;
     VMT_CUDA(cudaGetDevice(&dev));
-    const int slots = device_info(dev).sms * VMT_JUMP_MINB; // resident one-warp jobs
+    const int sms = device_info(dev).sms;
+    const int slots = sms * VMT_JUMP_MINB; // resident one-warp jobs
     const int n = jp.njobs;
+    // one wave instead of two: the 28-job-per-SM instantiation when it needs
+    // fewer waves than the 24-job one (each job ~2% slower)
+    auto waves = [&](int per_sm) { return (n + sms * per_sm - 1) / (sms * per_sm); };
     // measured on B200 (scratch/jump_bench.cu): split 8 wins below ~1/4 of the
     // warp slots, split 1 from 1/2 upwards
-    if (n >= slots / 2)
+    if (n >= slots / 2 && waves(28) < waves(VMT_JUMP_MINB))
+        vmt_jump_kernel<1, 28><<<n, 32, 0, st>>>(jp);
+    else if (n >= slots / 2)
         vmt_jump_kernel<1><<<n, 32, 0, st>>>(jp);
     else if (n >= slots / 4)
         vmt_jump_kernel<4><<<n, 128, 0, st>>>(jp);
@@ -812,10 +831,11 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     // GEMM than the serial GEMM costs (measured 6.53 vs 6.37 ms per 2^34
     // words).
     const int per_sm = (int)((grid + sms - 1) / (std::uint64_t)sms);
+    int pref_stages = 0;
     const bool tc_pref = h->prefetch == VMT_PREFETCH_TENSOR && h->positioning != 1 && h->gemm &&
                          mode != MODE_XOR && C * h->L >= gemm_min_rows() &&
                          (grid <= (std::uint64_t)sms || grid % sms == 0) && per_sm <= occ &&
-                         posmma_fits(h->device, fn, v.NT, smem, per_sm);
+                         (pref_stages = posmma_fits(h->device, fn, v.NT, smem, per_sm)) > 0;
     if ((h->prefetch == VMT_PREFETCH_JUMPS || tc_pref) && C > 1 && n >= kPrefetchMinWords) {
         const std::uint64_t gap = (h->last_end != ~0ull && P0 >= h->last_end) ? P0 - h->last_end : 0;
         const std::uint64_t P0n = P1 + gap;
@@ -887,7 +907,8 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
             // a cached matrix for the delta or for a base at most 4 blocks below
             // it (the rest regenerated in place, as in gemm_position)
             const std::uint64_t delta = next_b0 - b0, base = usable_base(*h->gemm, delta);
-            if (base && posmma_launch(*h->gemm, base, h->chunks.p, h->chunks_alt.p, h->L, C * h->L, sms, h->side)) {
+            if (base && posmma_launch(*h->gemm, base, h->chunks.p, h->chunks_alt.p, h->L, C * h->L, sms, h->side,
+                                      pref_stages)) {
                 if (delta > base) {
                     vmt_advance_blocks_kernel<<<(unsigned)((C * h->L + kAdvWarps - 1) / kAdvWarps), 32 * kAdvWarps,
                                                 0, h->side>>>(h->chunks_alt.p, (int)h->L, (long long)(C * h->L),

@@ -180,11 +180,15 @@ __device__ __forceinline__ void jump_load20(const std::uint32_t* seq, int start,
 // own copy of the sequence to the slice start) and the partial results are
 // XOR-reduced through shared memory -- SPLIT > 1 trades ~10% extra work for a
 // SPLIT-fold shorter latency when there are few jobs.
+// MINB: one-warp jobs resident per SM (the register cap): 24 = 77 registers,
+// no spills; 28 = 72 registers, one wave for up to 28 jobs per SM (config 5's
+// 4096 jobs on 148 SMs: 4.99 vs 5.39 ms over three launches); 32 = 64
+// registers with spills, 4% slower per job.
 #ifndef VMT_JUMP_MINB
-#define VMT_JUMP_MINB 24 // 77 registers, no spills (32: 64 registers + spills, 4% slower)
+#define VMT_JUMP_MINB 24
 #endif
-template <int SPLIT>
-__global__ void __launch_bounds__(32 * SPLIT, (SPLIT == 1 ? VMT_JUMP_MINB : 32 / SPLIT)) vmt_jump_kernel(JumpParams p) {
+template <int SPLIT, int MINB = VMT_JUMP_MINB>
+__global__ void __launch_bounds__(32 * SPLIT, (SPLIT == 1 ? MINB : 32 / SPLIT)) vmt_jump_kernel(JumpParams p) {
     __shared__ __align__(16) std::uint32_t seq_all[SPLIT][kSeqRing];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int job = blockIdx.x;

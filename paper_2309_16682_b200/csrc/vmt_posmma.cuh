@@ -277,9 +277,15 @@ __global__ void __launch_bounds__(kPmThreads, 1)
 // the generation kernel (§4.6).
 constexpr int kP2BQ = kPmNH / 2;                    // 104 B rows per CTA per MMA
 constexpr int kP2BQBytes = kP2BQ * kPmKE / 2;       // 6656
-constexpr int kP2Stages = 4;
 constexpr int kP2StageBytes = kPmABytes + 2 * kP2BQBytes; // 21504
-constexpr int kP2Smem = kP2Stages * kP2StageBytes + 1024 + 128;
+// Operand-ring depth: 4 stages (87 KB) fit beside a 108 KB generation CTA on
+// one SM (the co-resident prefetch); standalone launches (serial
+// positioning, batch de-phasing) and the smaller generation CTAs take deeper
+// rings, which hide more of the TMA latency of the B operand (200 MB, streamed
+// from HBM: it does not fit in L2).
+constexpr int kP2Stages = 4;
+__host__ __device__ constexpr int p2_smem(int stages) { return stages * kP2StageBytes + 1024 + 128; }
+constexpr int kP2Smem = p2_smem(kP2Stages);
 // kind::mxf4, M = 256 (pair), N = 208
 constexpr unsigned kP2Idesc = (1u << 7) | (1u << 10) | ((unsigned)(kPmNH >> 3) << 17) | (1u << 23) |
                               ((256u >> 4) << 24);
@@ -327,15 +333,16 @@ __device__ __forceinline__ void tc_mma_mxf4_pair(unsigned tmem_d, unsigned long 
 }
 
 // p.m_tiles = ceil(rows / 256) pair tiles; tmap_b boxes are 104 rows
+template <int kStages>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPmThreads, 1)
     vmt_posmma2_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                        const PosMmaParams p) {
     extern __shared__ unsigned char pm_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(pm_raw) + 1023) &
                                                            ~static_cast<std::uintptr_t>(1023));
-    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + kP2Stages * kP2StageBytes);
-    unsigned long long* empty = full + kP2Stages;
-    unsigned long long* accf = empty + kP2Stages; // MMA -> epilogues (both CTAs)
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + kStages * kP2StageBytes);
+    unsigned long long* empty = full + kStages;
+    unsigned long long* accf = empty + kStages; // MMA -> epilogues (both CTAs)
     unsigned long long* accd = accf + 1;           // epilogues (both CTAs) -> leader's MMA thread
     unsigned* tmem_slot = reinterpret_cast<unsigned*>(accd + 1);
 
@@ -343,7 +350,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPmThreads, 1)
     const unsigned rank = cluster_rank();
     const bool leader = rank == 0;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kP2Stages; ++s) {
+        for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);  // leader: its producer's expect_tx for both CTAs' bytes
             mbar_init(&empty[s], 1); // MMA commit, multicast to both CTAs
         }
@@ -386,8 +393,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPmThreads, 1)
             for (int tile = pair; tile < ntiles; tile += npairs) {
                 const int n = tile / p.m_tiles, m = tile % p.m_tiles;
                 for (int ks = 0; ks < kPmKSteps; ++ks, ++it) {
-                    const int s = it % kP2Stages;
-                    const unsigned u = it / kP2Stages;
+                    const int s = it % kStages;
+                    const unsigned u = it / kStages;
                     if (u > 0)
                         mbar_wait_parity(&empty[s], (u - 1) & 1);
                     unsigned char* a = smem + s * kP2StageBytes;
@@ -411,8 +418,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPmThreads, 1)
                     tc_fence_after();
                 }
                 for (int ks = 0; ks < kPmKSteps; ++ks, ++it) {
-                    const int s = it % kP2Stages;
-                    mbar_wait_parity(&full[s], (it / kP2Stages) & 1);
+                    const int s = it % kStages;
+                    mbar_wait_parity(&full[s], (it / kStages) & 1);
                     tc_fence_after();
                     const unsigned a = smem_u32(smem + s * kP2StageBytes);
                     const unsigned b = a + kPmABytes;
