@@ -69,11 +69,39 @@ def parse():
 
 
 # ----------------------------------------------------------------- clocks --
+_POLLER = r"""
+import sys, time
+import pynvml as nv
+nv.nvmlInit()
+key = sys.argv[1]
+try:
+    h = nv.nvmlDeviceGetHandleByUUID(key)
+except Exception:
+    h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[2]))
+get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
+mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+print("ready", flush=True)
+i = 0
+while True:
+    w = ""
+    if i % 4 == 0:
+        try:
+            w = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+        except Exception:
+            pass
+    i += 1
+    print(f"{time.monotonic():.6f},{nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)},{mx},{int(get_reasons(h))},{w}",
+          flush=True)
+    time.sleep(0.005)
+"""
+
+
 class ClockSampler:
-    """SM clocks and clock-event (throttle) reasons sampled DURING the timed
-    region: an NVML poller thread every 5 ms (the timed region of a default
-    run is well under a second, too short for `nvidia-smi -lms`), with the
-    recipe's nvidia-smi query as the fallback when NVML is unusable."""
+    """SM clocks, power and clock-event (throttle) reasons sampled DURING the
+    timed region: a separate NVML poller PROCESS (every ~5 ms, timestamped on
+    the system monotonic clock) so the sampling never waits on this process's
+    GIL while the timed loop launches work; only the samples between start()
+    and stop() are kept. Falls back to the recipe's nvidia-smi query."""
 
     # nvmlClocksEventReason* bits
     BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
@@ -84,65 +112,54 @@ class ClockSampler:
 
     def __init__(self, device):
         self.device = device
-        self.rows = []  # (sm_mhz, max_mhz, reasons bitmask)
+        self.rows = []  # (sm_mhz, max_mhz, reasons bitmask, watts or None)
         self.src = None
         self.proc = None
-        self.stop_flag = threading.Event()
-        self.nv = None
-        self.handle = None
+        self.lines = []
+        self.t0 = self.t1 = None
         try:
-            import pynvml as nv
             import torch
-            nv.nvmlInit()
             uuid = str(torch.cuda.get_device_properties(device).uuid)
-            try:
-                self.handle = nv.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
-            except Exception:
-                self.handle = nv.nvmlDeviceGetHandleByIndex(torch.device(device).index or 0)
-            self.nv = nv
+            uuid = uuid if uuid.startswith("GPU-") else "GPU-" + uuid
+            idx = torch.device(device).index or 0
+            self.proc = subprocess.Popen([sys.executable, "-c", _POLLER, uuid, str(idx)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            import atexit
+            atexit.register(self.proc.kill)
+            if self.proc.stdout.readline().strip() != "ready":  # NVML initialised, polling
+                raise RuntimeError("poller did not start")
+            self.reader = threading.Thread(target=self._drain, daemon=True)
+            self.reader.start()
+            self.src = "nvml poller process (~5 ms)"
         except Exception:
-            self.nv = None
+            if self.proc is not None:
+                self.proc.kill()
+            self.proc = None
 
-    def _poll(self):
-        nv, h = self.nv, self.handle
-        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
-            nv.nvmlDeviceGetCurrentClocksThrottleReasons
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-        i = 0
-        while True:
-            watts = None
-            if i % 8 == 0:  # (the power query is slower than the clock queries)
-                try:
-                    watts = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
-                except Exception:
-                    pass
-            i += 1
-            self.rows.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)), float(mx), int(get_reasons(h)),
-                              watts))
-            if self.stop_flag.wait(0.005):
-                break
+    def _drain(self):
+        for line in self.proc.stdout:
+            self.lines.append(line)
 
     def start(self):
-        if self.nv is not None:
-            self.src = "nvml (5 ms)"
-            self.thread = threading.Thread(target=self._poll, daemon=True)
-            self.thread.start()
+        if self.proc is not None:
+            time.sleep(0.02)  # at least a few samples queued before the region
+            self.t0 = time.monotonic()
             return
         try:
             self.src = "nvidia-smi -lms 100"
             idx = getattr(self.device, "index", None) or 0
-            self.proc = subprocess.Popen(
+            self.smi = subprocess.Popen(
                 ["nvidia-smi", "-i", str(idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read_smi, daemon=True)
             self.thread.start()
         except Exception:
-            self.proc = None
+            self.smi = None
             self.src = None
 
     def _read_smi(self):
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.proc.stdout:
+        for line in self.smi.stdout:
             r = [x.strip() for x in line.split(",")]
             if len(r) < 8 or not r[0].replace(".", "").isdigit():
                 continue
@@ -160,15 +177,29 @@ class ClockSampler:
         if self.src is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"], "samples": 0}
         if self.proc is not None:
-            time.sleep(0.25)
+            self.t1 = time.monotonic()
+            time.sleep(0.02)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
             except Exception:
                 self.proc.kill()
+            self.reader.join(timeout=2)
+            for line in list(self.lines):
+                r = line.strip().split(",")
+                try:
+                    t = float(r[0])
+                except (ValueError, IndexError):
+                    continue
+                if self.t0 <= t <= self.t1:
+                    self.rows.append((float(r[1]), float(r[2]), int(r[3]), float(r[4]) if r[4] else None))
         else:
-            self.stop_flag.set()
-            self.thread.join(timeout=2)
+            time.sleep(0.25)
+            self.smi.terminate()
+            try:
+                self.smi.wait(timeout=2)
+            except Exception:
+                self.smi.kill()
         rows = list(self.rows)
         reasons = sorted({nm for _, _, bits, _ in rows for nm, b in self.BITS.items() if bits & b})
         watts = [r[3] for r in rows if r[3] is not None]

@@ -10,7 +10,8 @@ import ctypes
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libvmt19937_b200.so")
+# VMT_LIB: A/B experiments only (another build of the same sources)
+LIB_PATH = os.environ.get("VMT_LIB") or os.path.join(PKG, "libvmt19937_b200.so")
 
 VMT_OK, VMT_EINVAL, VMT_ESTATE, VMT_EIO, VMT_ECUDA, VMT_ENOMEM = 0, -1, -2, -3, -4, -5
 VMT_FULL_PERIOD = 0xFFFFFFFF

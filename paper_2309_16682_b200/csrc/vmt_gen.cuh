@@ -89,9 +89,17 @@ struct GenShape {
     static constexpr int Q = L / V;            // threads across a slot row
     static constexpr int RUNS = W / R;         // runs per window
     static constexpr int NT = RUNS * Q;        // threads per CTA
-    static constexpr int RING = kN + W;        // ring slots
+    // In-place ring (the history-register shapes): slot = position mod 624,
+    // so every ring address is a per-thread constant + an immediate and the
+    // block loop needs no slot arithmetic; the one operand a neighbouring run
+    // overwrites in the same window (x_{p+R}, the next run's first word) is
+    // published one window ahead in a double-buffered exchange row instead.
+    static constexpr bool INPLACE = !TMA && kN % W == 0 && kN / W == 3 && R * V <= 26 && R >= 4;
+    static constexpr int RING = INPLACE ? kN : kN + W; // ring slots
     static constexpr int SLOTS = RING + R;     // + mirror of slots [0, R)
     static constexpr int RING_BYTES = SLOTS * L * 4;
+    static constexpr int BND_BYTES = INPLACE ? 2 * (RUNS + 1) * L * 4 : 0; // [parity][run 0..RUNS][lane]
+    static constexpr int EXTRA_OFF = RING_BYTES + BND_BYTES; // staging / histograms
     template <int MODE>
     __host__ __device__ static constexpr int stage_bytes() {
         return (TMA && staged_mode<MODE>()) ? W * L * elem_bytes<MODE>() : 0;
@@ -104,7 +112,7 @@ struct GenShape {
     }
     template <int MODE>
     __host__ __device__ static constexpr int smem() {
-        return RING_BYTES + stage_bytes<MODE>() + (stage_bytes<MODE>() ? 16 : 0) + hist_bytes<MODE>(); // + mbarrier
+        return EXTRA_OFF + stage_bytes<MODE>() + (stage_bytes<MODE>() ? 16 : 0) + hist_bytes<MODE>(); // + mbarrier
     }
     // CTAs per SM that shared memory allows (227 KB usable, 1 KB reserved per CTA)
     template <int MODE>
@@ -122,7 +130,13 @@ struct GenShape {
 #endif
         return (L == 32 && NT == 256 && MODE != MODE_XOR && MODE != MODE_STATS)
                    ? 1
+                   : (smem_ctas<MODE>() > reg_ctas()) ? reg_ctas()
                    : (smem_ctas<MODE>() * NT > 2048) ? (2048 / NT > 0 ? 2048 / NT : 1) : smem_ctas<MODE>();
+    }
+    // CTAs per SM that leave >= 128 registers per thread (the history shapes
+    // spill below that: 96 registers at 10 x 64 threads cost 2x at L=8)
+    __host__ __device__ static constexpr int reg_ctas() {
+        return 65536 / (NT * 128) > 0 ? 65536 / (NT * 128) : 1;
     }
     // Thread count the register allocation is bounded for (launch_bounds'
     // first argument; the kernel still launches NT threads).
@@ -134,6 +148,7 @@ struct GenShape {
         return NT;
     }
     static_assert(W % R == 0 && kN % W == 0 && RING % R == 0 && W <= 227, "bad window / run length");
+    static_assert(!INPLACE || kN - kM >= W, "in place: a window's x_{p+397} reads precede its writes");
     static_assert(!TMA || RING_BYTES % 16 == 0, "staging alignment");
 };
 
@@ -379,6 +394,88 @@ __device__ __forceinline__ void gen_window(std::uint32_t* ring, int base, int a,
     }
 }
 
+// One row of V new (untempered) words: fold / count / temper + emit (the
+// consumers of gen_window_ip; gen_window keeps its own copy for the staged
+// and paired-store forms). o points at the element of stream word g.
+template <int LT, int V, int MODE, bool VEC, bool FULL>
+__device__ __forceinline__ void consume_row(const std::uint32_t (&nw)[V], unsigned long long g, const GenParams& p,
+                                            typename ElemT<MODE>::T* o, std::uint32_t* acc, StageCtl& sc) {
+    if (MODE == MODE_XOR) {
+        // temper is GF(2)-linear: XOR the untempered words, temper once at the
+        // end (vmt_xor_reduce_kernel)
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+            if (FULL || (g + v >= p.pos_begin && g + v < p.pos_end))
+                acc[v] ^= nw[v];
+    } else if (MODE == MODE_STATS) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            if (FULL || (g + v >= p.pos_begin && g + v < p.pos_end)) {
+                const std::uint32_t t = temper(nw[v]);
+                acc[0] += __popc(t);
+                atomicAdd(sc.hist + (__byte_perm(t, 0u, 0x4440u) << 5), 1u);
+                atomicAdd(sc.hist + (__byte_perm(t, 0u, 0x4441u) << 5), 1u);
+                atomicAdd(sc.hist + (__byte_perm(t, 0u, 0x4442u) << 5), 1u);
+                atomicAdd(sc.hist + (__byte_perm(t, 0u, 0x4443u) << 5), 1u);
+            }
+        }
+    } else if (MODE == MODE_BENCH_TEMPER_XOR) {
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+            acc[v] ^= temper(nw[v]);
+    } else {
+        std::uint32_t tw[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+            tw[v] = temper(nw[v]);
+        emit<MODE, V, VEC, FULL>(tw, g, p, o);
+    }
+}
+
+// One window of one thread, in-place ring (GenShape::INPLACE). The run's x_p
+// .. x_{p+R-1} are its history registers H, x_{p+R} comes from the exchange
+// row bnd_rd (published by the next run one window earlier), x_{p+397} from
+// slots arow.. (mod 624, mirror behind the ring end); the new words go to the
+// run's own slots wslot.. (all ring loads of the window precede its stores
+// and no thread reads those slots in this window). o: the element of stream
+// word g0 (row i at o + i*LT, halved for two-word values).
+template <int LT, int L, int R, int V, int RING, int MODE, bool VEC, bool FULL>
+__device__ __forceinline__ void gen_window_ip(std::uint32_t* ring, int arow, int wslot, int q,
+                                              const std::uint32_t* bnd_rd, unsigned long long g0,
+                                              const GenParams& p, typename ElemT<MODE>::T* o, std::uint32_t* acc,
+                                              StageCtl& sc, std::uint32_t (&H)[R][V]) {
+    using VT = typename VecT<V>::T;
+    std::uint32_t X[R + 1][V], M[R][V];
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+            X[i][v] = H[i][v];
+    VecT<V>::get(*reinterpret_cast<const VT*>(bnd_rd), X[R]);
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+        VecT<V>::get(*reinterpret_cast<const VT*>(ring + (arow + i) * L + q * V), M[i]);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        std::uint32_t nw[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+            nw[v] = twist(X[i][v], X[i + 1][v], M[i][v]);
+        *reinterpret_cast<VT*>(ring + (wslot + i) * L + q * V) = VecT<V>::make(nw);
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+            H[i][v] = nw[v];
+        consume_row<LT, V, MODE, VEC, FULL>(nw, g0 + (unsigned long long)i * LT, p,
+                                            o + (MODE == MODE_F64_RES53 ? (i * LT) / 2 : i * LT), acc, sc);
+    }
+    if (wslot == 0) {
+        // mirror of slots [0, R) behind the ring end
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+            *reinterpret_cast<VT*>(ring + (RING + i) * L + q * V) = VecT<V>::make(H[i]);
+    }
+}
+
 // dst is the stream's [624][LT] state; this CTA's lanes are columns
 // [col0, col0 + L).
 template <int LT, int L, int RING>
@@ -430,12 +527,12 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::template lb_thread
                                  (MODE == MODE_F64_RES53 ? p.out_chunk_stride / 2 : p.out_chunk_stride) * chunk);
 
     StageCtl sc;
-    sc.buf = reinterpret_cast<unsigned char*>(ring) + S::RING_BYTES;
+    sc.buf = reinterpret_cast<unsigned char*>(ring) + S::EXTRA_OFF;
     sc.bar = reinterpret_cast<unsigned long long*>(sc.buf + S::template stage_bytes<MODE>());
     sc.phase = 0;
     sc.prev_staged = false;
     sc.pending = false;
-    sc.hist = reinterpret_cast<std::uint32_t*>(reinterpret_cast<unsigned char*>(ring) + S::RING_BYTES) +
+    sc.hist = reinterpret_cast<std::uint32_t*>(reinterpret_cast<unsigned char*>(ring) + S::EXTRA_OFF) +
               (MODE == MODE_STATS ? (tid & 31) : 0);
     // bulk copies need the window's destination 16-byte aligned
     const bool tma_ok =
@@ -456,7 +553,7 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::template lb_thread
         red = 0;
     __shared__ unsigned long long ones_red;
     if (MODE == MODE_STATS) {
-        std::uint32_t* h0 = reinterpret_cast<std::uint32_t*>(reinterpret_cast<unsigned char*>(ring) + S::RING_BYTES);
+        std::uint32_t* h0 = reinterpret_cast<std::uint32_t*>(reinterpret_cast<unsigned char*>(ring) + S::EXTRA_OFF);
         for (int i = tid; i < S::template hist_bytes<MODE>() / 4; i += S::NT)
             h0[i] = 0;
         if (tid == 0)
@@ -489,6 +586,68 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::template lb_thread
             for (int i = 0; i < R; ++i)
                 VecT<V>::get(*reinterpret_cast<const VT*>(ring + (wi * W + rho * R + i) * L + q * V), H[wi][i]);
     }
+    static_assert(!S::INPLACE || kHist, "the in-place ring needs the history registers");
+    if constexpr (S::INPLACE) {
+        // ---- in-place ring: static slots, one range check per block ----
+        constexpr int BROW = (S::RUNS + 1) * L; // exchange words per parity
+        std::uint32_t* const bnd = ring + S::SLOTS * L;
+        const int r0 = rho * R;
+        int arow[kWins];
+#pragma unroll
+        for (int wi = 0; wi < kWins; ++wi) {
+            const int a = wi * W + r0 + kM;
+            arow[wi] = a >= kN ? a - kN : a;
+        }
+        // the first window's x_{p+R} words (parity 0)
+        *reinterpret_cast<VT*>(bnd + rho * L + q * V) = VecT<V>::make(H[0][0]);
+        if (rho == 0)
+            *reinterpret_cast<VT*>(bnd + S::RUNS * L + q * V) = VecT<V>::make(H[1][0]);
+        __syncthreads();
+        int par = 0;
+        constexpr int kShift = MODE == MODE_F64_RES53 ? 1 : 0; // two stream words per value
+        E* const out_e = static_cast<E*>(out);
+        for (unsigned long long blk = b_lo; blk < b_hi; ++blk) {
+            if (save_here && blk == p.save_block)
+                save_boundary<LT, L, S::RING>(ring, 0, save_dst, col0, tid, S::NT);
+            const unsigned long long gb = blk * bw; // first stream word of the block
+            const bool bfull = gb >= p.pos_begin && gb + bw <= p.pos_end;
+            const unsigned long long g_thr = gb + (unsigned long long)r0 * LT + col0 + q * V;
+            // element of this thread's first word in the block (full blocks only)
+            E* const o_blk = out_e + (bfull ? ((g_thr - p.pos_begin) >> kShift) : 0ull);
+#pragma unroll
+            for (int wi = 0; wi < kWins; ++wi) {
+                // publish the next window's x_{p+R} words (the other parity)
+                std::uint32_t* const bw_row = bnd + (par ^ 1) * BROW;
+                *reinterpret_cast<VT*>(bw_row + rho * L + q * V) = VecT<V>::make(H[(wi + 1) % kWins][0]);
+                if (rho == 0)
+                    *reinterpret_cast<VT*>(bw_row + S::RUNS * L + q * V) = VecT<V>::make(H[(wi + 2) % kWins][0]);
+                const std::uint32_t* const bnd_rd = bnd + par * BROW + (rho + 1) * L + q * V;
+                const unsigned long long g0 = g_thr + (unsigned long long)wi * ww;
+                if (bfull) {
+                    gen_window_ip<LT, L, R, V, S::RING, MODE, VEC, true>(
+                        ring, arow[wi], wi * W + r0, q, bnd_rd, g0, p, o_blk + ((wi * ww) >> kShift), acc, sc, H[wi]);
+                } else {
+                    const unsigned long long gw = gb + (unsigned long long)wi * ww;
+                    // (as gen_window: words before pos_begin wrap modulo 2^64 and are never stored)
+                    E* const o = out_e + ((g0 - p.pos_begin) >> kShift);
+                    if (gw >= p.pos_begin && gw + ww <= p.pos_end)
+                        gen_window_ip<LT, L, R, V, S::RING, MODE, VEC, true>(ring, arow[wi], wi * W + r0, q, bnd_rd,
+                                                                          g0, p, o, acc, sc, H[wi]);
+                    else
+                        gen_window_ip<LT, L, R, V, S::RING, MODE, VEC, false>(ring, arow[wi], wi * W + r0, q, bnd_rd,
+                                                                           g0, p, o, acc, sc, H[wi]);
+                }
+                par ^= 1;
+                __syncthreads();
+                if (MODE == MODE_STATS) {
+                    ones += acc[0];
+                    acc[0] = 0;
+                }
+            }
+        }
+        if (save_here && b_hi == p.save_block && b_hi == p.end_block)
+            save_boundary<LT, L, S::RING>(ring, 0, save_dst, col0, tid, S::NT);
+    } else {
     auto window = [&](unsigned long long blk, int wi, std::uint32_t (&Hw)[R][V]) {
         {
             int wstart = blk_base_slot + wi * W;
@@ -553,6 +712,7 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::template lb_thread
     // end-of-range boundary state (block b_hi) when it is the requested one
     if (save_here && b_hi == p.save_block && b_hi == p.end_block)
         save_boundary<LT, L, S::RING>(ring, blk_base_slot, save_dst, col0, tid, S::NT);
+    } // !INPLACE
     if (kStaged && tid == 0 && sc.pending)
         bulk_wait_all(); // the staging buffer must outlive the last bulk copy
     if (kFold) {
@@ -569,7 +729,7 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::template lb_thread
         // (every window ended with a barrier: the histograms are complete)
         atomicAdd(&ones_red, ones);
         const std::uint32_t* h0 =
-            reinterpret_cast<const std::uint32_t*>(reinterpret_cast<unsigned char*>(ring) + S::RING_BYTES);
+            reinterpret_cast<const std::uint32_t*>(reinterpret_cast<unsigned char*>(ring) + S::EXTRA_OFF);
         unsigned long long* dst = p.stats_partials + (unsigned long long)blockIdx.x * kStatWords;
         for (int b = tid; b < 256; b += S::NT) {
             unsigned long long c = 0;

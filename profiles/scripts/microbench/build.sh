@@ -13,3 +13,9 @@ $NV -DMB_TMA=true -o $D/_bin/mb_tma208 $D/mb_gen.cu
 $NV -DVMT_PAIR128=1 -o $D/_bin/mb_pair128 $D/mb_gen.cu
 $NV -DNC=256 -DCV=2 -o $D/_bin/ws_256 $D/ws_gen.cu
 $NV -o $D/_bin/probe_st $D/probe_st.cu
+$NV -o $D/_bin/pipes $D/pipes.cu                                      # pipe rates (pipes.log)
+$NV -DSV=4 -o $D/_bin/split_v4 $D/split_gen.cu                        # runs of 6/7, 4 lanes per thread
+$NV -DSV=2 -o $D/_bin/split_v2 $D/split_gen.cu                        # runs of 6/7, 512 threads
+$NV -o $D/_bin/inplace $D/inplace_gen.cu                              # in-place ring, static slots
+$NV -o $D/_bin/probe_power $D/probe_power.cu                          # store paths: rate + power (power.sh)
+$NV -DSTAGE=1 -o $D/_bin/inplace_tma $D/inplace_gen.cu                  # + TMA bulk stores of double-buffered windows

@@ -57,8 +57,11 @@ int main(int argc, char** argv) {
     p.chunk_states = states; p.out = out; p.xor_partials = parts; p.save_state = nullptr;
     p.first_block = 0; p.end_block = C * B; p.pos_begin = 0; p.pos_end = n; p.save_block = ~0ull;
     p.blocks_per_chunk = (unsigned)B; p.lanes = L;
-    const float ms_store = run<MODE_U32>(p, C, reps, st);
-    const float ms_xor = run<MODE_BENCH_TEMPER_XOR>(p, C, reps, st);
+    // MB_ONLY=store / MB_ONLY=xor: run one of the two (power sampling)
+    const char* only = getenv("MB_ONLY");
+    const bool do_store = !only || only[0] == 's', do_xor = !only || only[0] == 'x';
+    const float ms_store = do_store ? run<MODE_U32>(p, C, reps, st) : 0.f;
+    const float ms_xor = do_xor ? run<MODE_BENCH_TEMPER_XOR>(p, C, reps, st) : 0.f;
     std::vector<unsigned> hp(C);
     CK(cudaMemcpy(hp.data(), parts, C * 4, cudaMemcpyDeviceToHost));
     unsigned x = 0; for (auto v : hp) x ^= v;

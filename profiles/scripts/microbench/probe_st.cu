@@ -27,6 +27,12 @@ int main(int argc, char** argv) {
     const int reps = argc > 1 ? atoi(argv[1]) : 20;
     const unsigned long long bytes = 16ull << 30;
     void* p; cudaMalloc(&p, bytes);
+    if (argc > 2) { // one probe only (power sampling): v4 or v2, 148 x 256
+        const bool v4 = argv[2][1] == '4';
+        const float t = v4 ? run((uint4*)p, bytes, 148, 256, reps) : run((uint2*)p, bytes, 148, 256, reps);
+        printf("{\"reps\": %d, \"%s_148x256\": %.3f}\n", reps, argv[2], t);
+        return 0;
+    }
     printf("{\"reps\": %d, \"v4_148x256\": %.3f, \"v2_148x256\": %.3f, \"v4_296x256\": %.3f, \"v4_148x512\": %.3f}\n", reps,
            run((uint4*)p, bytes, 148, 256, reps), run((uint2*)p, bytes, 148, 256, reps),
            run((uint4*)p, bytes, 296, 256, reps), run((uint4*)p, bytes, 148, 512, reps));
