@@ -684,7 +684,10 @@ def main():
     store_peaks = {}
     try:
         store_peaks = {"grid_stride_gbs": V.store_bandwidth(count * 4, 0, 2, local),
-                       "chunk_per_cta_gbs": V.store_bandwidth(count * 4, 1, 1, local)}
+                       "chunk_per_cta_gbs": V.store_bandwidth(count * 4, 1, 1, local),
+                       # random words, like the generator's output: the HBM interface power of
+                       # the store stream alone approaches the board's 1000 W limit (DESIGN 4.1)
+                       "chunk_per_cta_random_gbs": V.store_bandwidth(count * 4, 2, 1, local)}
     except Exception as e:
         store_peaks = {"error": str(e)}
     bytes_per_launch = count * 4

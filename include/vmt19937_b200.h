@@ -295,8 +295,9 @@ int vmt_regularized_gamma_q(double a, double x, double* out);
 
 /* Measurement only: GB/s of a pure 16-byte-store kernel over `bytes` of HBM,
  * pattern 0 = grid-stride, 1 = one contiguous chunk per CTA (the generation
- * kernel's output pattern); grid = SMs x ctas_per_sm. The second roofline
- * denominator next to MEASURED_PEAKS.json's copy bandwidth. */
+ * kernel's output pattern), 2 = as 1 with random-looking words (HBM interface
+ * power depends on the bits toggled); grid = SMs x ctas_per_sm. The second
+ * roofline denominator next to MEASURED_PEAKS.json's copy bandwidth. */
 int vmt_store_bandwidth(int device, uint64_t bytes, int pattern, int ctas_per_sm, double* gbs);
 
 const char* vmt_status_string(int status);

@@ -388,7 +388,8 @@ def release_caches(device: int = 0) -> None:
 
 
 def store_bandwidth(bytes_: int = 1 << 34, pattern: int = 0, ctas_per_sm: int = 2, device: int = 0) -> float:
-    """GB/s of a pure-store probe kernel (0 grid-stride, 1 chunk per CTA)."""
+    """GB/s of a pure-store probe kernel (0 grid-stride, 1 chunk per CTA, 2 chunk
+    per CTA with random-looking words)."""
     out = ctypes.c_double()
     check(lib.vmt_store_bandwidth(device, bytes_, pattern, ctas_per_sm, ctypes.byref(out)))
     return out.value

@@ -1705,7 +1705,8 @@ int vmt_stats(vmt_handle h, uint64_t* gen_launches, uint64_t* jump_launches, uin
 int vmt_store_bandwidth(int device, uint64_t bytes, int pattern, int ctas_per_sm, double* gbs) {
     return guarded([&] {
         require(gbs != nullptr && bytes >= 16, VMT_EINVAL, "bad argument");
-        require(pattern == 0 || pattern == 1, VMT_EINVAL, "pattern must be 0 (grid-stride) or 1 (chunked)");
+        require(pattern >= 0 && pattern <= 2, VMT_EINVAL,
+                "pattern must be 0 (grid-stride), 1 (chunked) or 2 (chunked, random words)");
         check_device(device);
         DeviceGuard g(device);
         const unsigned long long n4 = bytes / 16;
@@ -1717,8 +1718,10 @@ int vmt_store_bandwidth(int device, uint64_t bytes, int pattern, int ctas_per_sm
         auto launch = [&] {
             if (pattern == 0)
                 vmt_store_probe_stride<<<grid, 512, 0, st>>>(buf.p, n4);
-            else
+            else if (pattern == 1)
                 vmt_store_probe_chunked<<<grid, 256, 0, st>>>(buf.p, n4);
+            else
+                vmt_store_probe_chunked_random<<<grid, 256, 0, st>>>(buf.p, n4);
         };
         launch();
         VMT_CUDA(cudaGetLastError());

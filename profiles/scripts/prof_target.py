@@ -9,6 +9,13 @@
   posmma: vmt_posmma2_kernel, the co-resident tcgen05 FP4 positioning GEMM (CTA pairs)
           (4736 lane states x F^(624 D)); under ncu it runs serialised, i.e.
           alone on the GPU (6 fills of 2^32 words; it launches from fill 3 on)
+  steady: the bench's steady state -- 2^34-word fills at L=32 with the
+          co-resident positioning prefetch; the 9th fill is bracketed by
+          cudaProfilerStart/Stop so `ncu --replay-mode app-range
+          --profile-from-start off` measures ONE whole step (generation kernel
+          + the next step's tcgen05 positioning GEMM running beside it)
+          with the kernels concurrent, as in the bench
+  c5    : config 5 as bench.py runs it (4096 seeded states, 64-bit jumps), 3 calls
   c1/c2/c3: the other BASELINE configs as bench.py's extras run them (8
           repeats of each call, past the one-time matrix builds) -- for the
           launch lists showing every kernel is ours
@@ -24,6 +31,31 @@ import paper_2309_16682_b200 as V  # noqa: E402
 
 what = sys.argv[1]
 n = 1 << 32
+if what == "c5":
+    import numpy as np
+    seeds = np.arange(1, 4097, dtype=np.uint32)
+    states = torch.from_numpy(V.seed_states(seeds).view(np.int32)).cuda().view(torch.uint32)
+    dists = np.random.default_rng(7).integers(0, 2**63, 4096, dtype=np.int64).view(np.uint64)
+    jumped = torch.empty_like(states)
+    for _ in range(3):
+        V.jump_states(states, dists, out=jumped)
+    torch.cuda.synchronize()
+    print("done", what)
+    sys.exit(0)
+if what == "steady":
+    g = V.VmtGenerator(5489, V.VmtConfig(32))
+    buf = torch.empty(1 << 34, dtype=torch.uint32, device="cuda")
+    for _ in range(8):
+        g.fill_u32(buf)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
+    g.fill_u32(buf)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
+    st = g.prefetch_stats()
+    assert st["tensor_prefetches"] >= 6, st
+    print("done", what, st)
+    sys.exit(0)
 if what in ("c1", "c2", "c3"):
     if what == "c1":
         g = V.VmtGenerator(5489, V.VmtConfig(16))
