@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--no-extras", action="store_true", help="skip the other BASELINE configs (N=1 only)")
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--chunks", type=int, default=0)
+    ap.add_argument("--prefetch", type=int, default=2, choices=[0, 1, 2],
+                    help="positioning prefetch: 2 the co-resident tcgen05 GEMM (default), 1 jumps on a side "
+                         "stream, 0 off (serial positioning)")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                     help="weak: every rank generates its own 2^34-word share of an N*2^34-word stream "
                          "per step (the path shards with no data exchange); strong: one 2^34 stream "
@@ -499,6 +502,7 @@ def main():
     g = V.VmtGenerator(SEED, V.VmtConfig(LANES), device=local)  # seed + full-period de-phasing
     setup_ms = (time.perf_counter() - t_setup) * 1e3
     g.set_tuning(max_chunks=args.chunks, variant=args.variant)
+    g.set_prefetch(args.prefetch)
     out = torch.empty(count, dtype=torch.uint32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -562,7 +566,7 @@ def main():
         f1.synchronize()
         sf, sj, sg = g.profile_totals()
         g.set_profiling(False)
-        g.set_prefetch(2)
+        g.set_prefetch(args.prefetch)
         serial = {"ms_per_step": f0.elapsed_time(f1) / 3, "gen_kernel": sg / max(sf, 1),
                   "positioning": sj / max(sf, 1),
                   "gen_roofline_frac": count * 4 / (sg / max(sf, 1) * 1e-3) / 1e9 / measured_peak()[0],

@@ -195,13 +195,32 @@ __device__ __forceinline__ double to_f64_res53(std::uint32_t a, std::uint32_t b)
     return (__uint2double_rn(a >> 5) * 67108864.0 + __uint2double_rn(b >> 6)) * 1.1102230246251565e-16;
 }
 
+// Output stores (streamed once, never re-read by this kernel). Default 3: L2
+// evict-first policy, so the output stream does not push the co-resident
+// positioning GEMM's operands (the 47 MB FP4 state operand, read once per
+// output slice, and the 200 MB matrix) out of L2: in the driver's 20-step
+// shape 12.47-12.52 vs 12.72-12.81 ms per 2^34-word step, burst 11.30-11.34
+// vs 11.72 (profiles/r02_microbench/README.md). 1: st.global.cs (similar),
+// 0: plain.
 #ifndef VMT_STORE_HINT
-#define VMT_STORE_HINT 0
+#define VMT_STORE_HINT 3
 #endif
-// Output stores (streamed once, never re-read by this kernel).
 template <class VT>
 __device__ __forceinline__ void store_out(VT* p, const VT& v) {
     *p = v;
+}
+template <>
+__device__ __forceinline__ void store_out<uint2>(uint2* p, const uint2& v) {
+#if VMT_STORE_HINT == 3
+    unsigned long long pol; // (not volatile: one createpolicy per thread, hoisted)
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(v.x), "r"(v.y), "l"(pol)
+                 : "memory");
+#elif VMT_STORE_HINT == 1
+    __stcs(p, v);
+#else
+    *p = v;
+#endif
 }
 template <>
 __device__ __forceinline__ void store_out<uint4>(uint4* p, const uint4& v) {
@@ -212,8 +231,10 @@ __device__ __forceinline__ void store_out<uint4>(uint4* p, const uint4& v) {
                  "r"(v.w)
                  : "memory");
 #elif VMT_STORE_HINT == 3
-    asm volatile("st.global.L2::evict_first.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
-                 "r"(v.w)
+    unsigned long long pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w), "l"(pol)
                  : "memory");
 #else
     *p = v;
