@@ -318,7 +318,7 @@ def extras(dev) -> dict:
 
     stream = torch.cuda.current_stream(dev)
 
-    def timed(fn, reps=3, warm=8):
+    def timed(fn, reps=10, warm=8):
         # steady state: the warm calls include the one-time positioning-matrix
         # build of a repeating fill shape
         for _ in range(warm):

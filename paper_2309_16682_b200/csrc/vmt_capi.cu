@@ -709,7 +709,7 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
         const std::uint64_t e = (std::uint64_t)(a / (std::uintptr_t)esz);
         const int need = (esz == 8) ? 2 : V; // double2 / VecT<V> stores
         vec = (a % (std::uintptr_t)esz == 0) && ((e - P0) % (std::uint64_t)need == 0) && (P0 % V == 0) &&
-              (esz == 4 || V == 4);
+              (esz == 4 || V >= 2);
     }
     GenFn fn = v.fn[mode][vec ? 1 : 0];
     const int smem = v.smem[mode];

@@ -182,6 +182,8 @@ __device__ __forceinline__ void emit(const std::uint32_t* w, unsigned long long 
             f[v] = to_f32(w[v]);
         if (VEC && V == 4 && all_in) {
             *reinterpret_cast<float4*>(o) = make_float4(f[0], f[1], f[2], f[3]);
+        } else if (VEC && V == 2 && all_in) {
+            *reinterpret_cast<float2*>(o) = make_float2(f[0], f[1]);
         } else {
 #pragma unroll
             for (int v = 0; v < V; ++v)
@@ -196,6 +198,8 @@ __device__ __forceinline__ void emit(const std::uint32_t* w, unsigned long long 
         if (VEC && V == 4 && all_in) {
             reinterpret_cast<double2*>(o)[0] = make_double2(d[0], d[1]);
             reinterpret_cast<double2*>(o)[1] = make_double2(d[2], d[3]);
+        } else if (VEC && V == 2 && all_in) {
+            *reinterpret_cast<double2*>(o) = make_double2(d[0], d[1]);
         } else {
 #pragma unroll
             for (int v = 0; v < V; ++v)

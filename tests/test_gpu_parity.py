@@ -477,3 +477,35 @@ def test_config3_sampled_generators_vs_oracle(oracle, full_polys, seed):
     w = dev_u32(n)
     V.VmtGenerator(seed, V.VmtConfig(16)).fill_u32(w)
     assert np.array_equal(host(w), ref), seed
+
+
+@pytest.mark.parametrize("L", [8, 16, 32])
+def test_float_fills_ragged_and_misaligned(oracle, L):
+    """Float32 / float64 fills of ragged lengths into views at odd element
+    offsets: consecutive fills start at odd stream positions and write to
+    destinations that are not 8- / 16-byte aligned, so both the vector
+    (float2 / double2) and the scalar store paths run; every value must equal
+    the conversion rule applied to the oracle's stream."""
+    q = 16
+    sizes = [1001, 2048, 333, 70000 + 3, 1]
+    total = sum(sizes)
+    lanes = oracle.dephased_states(7, L, oracle.x_pow2_mod(q))
+    u = oracle.vmt_stream(lanes, 0, total)
+    ref32 = (u >> np.uint32(8)).astype(np.float32) * np.float32(2.0 ** -24)
+    ref64 = (u.astype(np.float64) + 0.5) * 2.0 ** -32
+    for kind, ref in (("f32", ref32), ("f64", ref64)):
+        g = V.VmtEngine(L, 7, q)
+        dt = torch.float32 if kind == "f32" else torch.float64
+        buf = torch.empty(total + 2 * len(sizes) + 1, dtype=dt, device="cuda")
+        pos, off, views = 0, 1, []
+        for k, sz in enumerate(sizes):
+            v = buf[off:off + sz]
+            if kind == "f32":
+                g.fill_f32(v)
+            else:
+                g.fill_f64(v, rule=V.VMT_F64_REAL3)
+            views.append((v, pos, sz))
+            pos += sz
+            off += sz + (k % 2)  # alternate parity of the next destination
+        for v, p0, sz in views:
+            assert np.array_equal(host(v), ref[p0:p0 + sz]), (kind, p0, sz)
