@@ -725,7 +725,14 @@ def main():
                      "kernel": "vmt_gen_kernel", "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_per_launch,
                      "store_probe": dict(store_peaks, frac_of_grid_stride=(
-                         achieved / store_peaks["grid_stride_gbs"] if "grid_stride_gbs" in store_peaks else None))},
+                         achieved / store_peaks["grid_stride_gbs"] if "grid_stride_gbs" in store_peaks else None)),
+                     "limited_by": (
+                         "board power limit (sw_power_cap during the timed steps): storing random words at "
+                         "~6.4 TB/s alone draws ~990 W of the 1000 W limit and twist + temper add ~210 pJ/word, so "
+                         "the SM clock is lowered until both fit (profiles/r02_summary.md)"
+                         if "sw_power_cap" in (clk.get("reasons") or []) else
+                         "ALU issue at full clock (twist + temper: 9 ALU-pipe ops per word, ALU pipe ~79%) beside "
+                         "the 64-bit output stores; DRAM traffic = the algorithmic bytes (roofline.traffic)")},
         "checksum_xor": f"0x{csum:08x}",
         "checksum_oracle": oracle_checksum(T, world, args),
         "clocks": clk,
