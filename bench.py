@@ -145,7 +145,6 @@ class ClockSampler:
 
     def start(self):
         if self.proc is not None:
-            time.sleep(0.02)  # at least a few samples queued before the region
             self.t0 = time.monotonic()
             return
         try:
@@ -513,6 +512,10 @@ def main():
             g.checksum_xor(count, stream=stream.cuda_stream or 1)
         g.skip(T - count)  # the other ranks' share of this step
 
+    # the clock/power poller starts before the warm-up, so the timed steps
+    # follow the warm-up steps without an idle gap (the board's power state
+    # is that of continuous load)
+    clocks = ClockSampler(dev)
     g.seek(start)
     for _ in range(args.warmup):
         step()
@@ -521,7 +524,6 @@ def main():
         dist.barrier()
     torch.cuda.synchronize(dev)
 
-    clocks = ClockSampler(dev)
     g.set_profiling(True)  # CUDA events around each step's jump and generation launches
     g.profile_totals()
     clocks.start()
