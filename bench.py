@@ -14,7 +14,10 @@ cached between steps). Output goes to a preallocated HBM buffer of the rank's
 share (64 GiB -- larger than L2, no flush needed).
 
 value    : whole-job uint32/s over all ranks, CUDA events on the launching
-           stream, max over ranks (positioning jumps + generation kernels).
+           stream, max over ranks (chunk positioning + generation kernels;
+           the positioning is the tcgen05 FP4 GEMM between the steps by
+           default, --prefetch 2 runs it beside the previous step's
+           generation kernel; the other mode is reported next to it).
 e2e      : the same workload through the public API into pinned HOST memory
            (device->host copy of every word inside the timed region).
 roofline : the generation kernel (vmt_gen_kernel) alone: algorithmic bytes
@@ -61,9 +64,13 @@ def parse():
     ap.add_argument("--no-extras", action="store_true", help="skip the other BASELINE configs (N=1 only)")
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--chunks", type=int, default=0)
-    ap.add_argument("--prefetch", type=int, default=2, choices=[0, 1, 2],
-                    help="positioning prefetch: 2 the co-resident tcgen05 GEMM (default), 1 jumps on a side "
-                         "stream, 0 off (serial positioning)")
+    ap.add_argument("--prefetch", type=int, default=0, choices=[0, 1, 2],
+                    help="positioning of each step's chunk states: 0 the tcgen05 FP4 GEMM between the steps "
+                         "(bench default), 2 the same GEMM co-resident with the previous step's generation "
+                         "kernel (the library default), 1 polynomial jumps on a side stream. Under the "
+                         "driver's power-capped 20-step run 0 and 2 differ by <1%% in step time (the GEMM's "
+                         "energy is spent either way); 0 keeps the generation kernel's roofline free of the "
+                         "GEMM beside it; the other mode is timed after the timed steps for comparison")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                     help="weak: every rank generates its own 2^34-word share of an N*2^34-word stream "
                          "per step (the path shards with no data exchange); strong: one 2^34 stream "
@@ -549,12 +556,12 @@ def main():
     gen_ms = max_over_ranks(gen_tot / max(fills, 1), coll)
     jump_ms = max_over_ranks(jump_tot / max(fills, 1), coll)
 
-    # -- the same steps with the serial positioning (no co-resident tcgen05
-    # prefetch): explains the split between the generation kernel's own
-    # roofline and the positioning it hides (reported, not the headline)
+    # -- the same steps with the other positioning mode (serial GEMM <->
+    # co-resident GEMM), reported beside the timed mode, not the headline
+    other_pf = 2 if args.prefetch == 0 else 0
     serial = None
     if args.mode == "store" and not args.no_extras:
-        g.set_prefetch(0)
+        g.set_prefetch(other_pf)
         for _ in range(2):
             step()
         torch.cuda.synchronize(dev)
@@ -569,10 +576,14 @@ def main():
         sf, sj, sg = g.profile_totals()
         g.set_profiling(False)
         g.set_prefetch(args.prefetch)
-        serial = {"ms_per_step": f0.elapsed_time(f1) / 3, "gen_kernel": sg / max(sf, 1),
+        serial = {"prefetch": other_pf, "ms_per_step": f0.elapsed_time(f1) / 3, "gen_kernel": sg / max(sf, 1),
                   "positioning": sj / max(sf, 1),
                   "gen_roofline_frac": count * 4 / (sg / max(sf, 1) * 1e-3) / 1e9 / measured_peak()[0],
-                  "note": "3 steps with vmt_set_prefetch(OFF): our tcgen05 FP4 GEMM between steps instead"}
+                  "note": ("3 steps after the timed ones with the tcgen05 FP4 positioning GEMM co-resident with "
+                           "the generation kernel (vmt_set_prefetch(2), the library default): its cost moves "
+                           "inside gen_kernel" if other_pf == 2 else
+                           "3 steps after the timed ones with vmt_set_prefetch(OFF): the tcgen05 FP4 GEMM between "
+                           "the steps")}
 
     # -- global checksum of one full 2^34 range (config 4 verification)
     g.seek(start)
@@ -715,13 +726,19 @@ def main():
         "timing_breakdown_ms": {"gen_kernel": gen_ms, "positioning": jump_ms, "setup_create": setup_ms,
                                 "positioning_gemms": g.positioning_stats()["gemm_positionings"],
                                 "prefetch": g.prefetch_stats(),
-                                "serial_positioning": serial,
+                                "positioning_mode": args.prefetch,
+                                "other_positioning_mode": serial,
                                 "note": "CUDA events on the fill's stream around the chunk positioning and the "
-                                        "generation launch of every timed step. Steady state: the next step's 4736 "
-                                        "chunk lane states are computed during this step's generation kernel by the "
-                                        "co-resident tcgen05 FP4 GEMM (vmt_posmma_kernel, on the idle tensor cores), "
-                                        "so 'positioning' is only the wait for it and its cost shows up inside "
-                                        "gen_kernel; first steps: polynomial jumps, then the serial tcgen05 FP4 GEMM"},
+                                        "generation launch of every timed step. " + (
+                                            "Steady state: each step's 4736 chunk lane states are one tcgen05 FP4 "
+                                            "GEMM (vmt_posmma2_kernel, 4736 x 19968^2, ~0.75 ms) launched before "
+                                            "the step's generation kernel ('positioning')"
+                                            if args.prefetch == 0 else
+                                            "Steady state: the next step's 4736 chunk lane states are computed "
+                                            "during this step's generation kernel by the co-resident tcgen05 FP4 "
+                                            "GEMM, so 'positioning' is only the wait for it and its cost shows up "
+                                            "inside gen_kernel") + "; first steps: polynomial jumps, then the GEMM "
+                                        "once the positioning matrix of the repeating step is built"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": (traffic or {}).get("dram_bytes_per_launch"),
                      "kernel": "vmt_gen_kernel", "peak_source": peak_src,
