@@ -182,11 +182,16 @@ class ClockSampler:
                 watts = None
             self.rows.append((float(r[0]), float(r[1]) if r[1].replace(".", "").isdigit() else 0.0, bits, watts))
 
+    def mark_end(self):
+        """End of the timed region (stop() may come later)."""
+        if self.t1 is None:
+            self.t1 = time.monotonic()
+
     def stop(self) -> dict:
         if self.src is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"], "samples": 0}
         if self.proc is not None:
-            self.t1 = time.monotonic()
+            self.mark_end()
             time.sleep(0.02)
             self.proc.terminate()
             try:
@@ -541,49 +546,50 @@ def main():
         step()
     e1.record(stream)
     e1.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    clk = clocks.stop()
+    clocks.mark_end()
     s1 = g.stats()
     fills, jump_tot, gen_tot = g.profile_totals()
     g.set_profiling(False)
-    ms = e0.elapsed_time(e1) / args.steps
-    ms = max_over_ranks(ms, coll)
-    launches = sum(s1[k] - s0[k] for k in ("gen_launches", "jump_launches", "other_launches"))
-    # the generation kernel's own duration and the positioning jumps before
-    # it, from the same timed steps
-    gen_ms = max_over_ranks(gen_tot / max(fills, 1), coll)
-    jump_ms = max_over_ranks(jump_tot / max(fills, 1), coll)
 
-    # -- the same steps with the other positioning mode (serial GEMM <->
-    # co-resident GEMM), reported beside the timed mode, not the headline
+    # -- the same number of steps with the other positioning mode (serial GEMM
+    # <-> co-resident GEMM), run straight after the timed steps so the board
+    # is in the same (power-capped) state; reported beside the timed mode
     other_pf = 2 if args.prefetch == 0 else 0
     serial = None
     if args.mode == "store" and not args.no_extras:
         g.set_prefetch(other_pf)
         for _ in range(2):
             step()
-        torch.cuda.synchronize(dev)
         g.set_profiling(True)
         g.profile_totals()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
-        for _ in range(3):
+        for _ in range(args.steps):
             step()
         f1.record(stream)
         f1.synchronize()
         sf, sj, sg = g.profile_totals()
         g.set_profiling(False)
         g.set_prefetch(args.prefetch)
-        serial = {"prefetch": other_pf, "ms_per_step": f0.elapsed_time(f1) / 3, "gen_kernel": sg / max(sf, 1),
-                  "positioning": sj / max(sf, 1),
+        serial = {"prefetch": other_pf, "steps": args.steps, "ms_per_step": f0.elapsed_time(f1) / args.steps,
+                  "gen_kernel": sg / max(sf, 1), "positioning": sj / max(sf, 1),
                   "gen_roofline_frac": count * 4 / (sg / max(sf, 1) * 1e-3) / 1e9 / measured_peak()[0],
-                  "note": ("3 steps after the timed ones with the tcgen05 FP4 positioning GEMM co-resident with "
-                           "the generation kernel (vmt_set_prefetch(2), the library default): its cost moves "
-                           "inside gen_kernel" if other_pf == 2 else
-                           "3 steps after the timed ones with vmt_set_prefetch(OFF): the tcgen05 FP4 GEMM between "
-                           "the steps")}
+                  "note": ("the tcgen05 FP4 positioning GEMM co-resident with the generation kernel "
+                           "(vmt_set_prefetch(2), the library default): its cost moves inside gen_kernel"
+                           if other_pf == 2 else
+                           "vmt_set_prefetch(OFF): the tcgen05 FP4 positioning GEMM between the steps") +
+                          "; run straight after the timed steps (2 more warm-up steps)"}
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    ms = max_over_ranks(ms, coll)
+    launches = sum(s1[k] - s0[k] for k in ("gen_launches", "jump_launches", "other_launches"))
+    # the generation kernel's own duration and the positioning before it,
+    # from the same timed steps
+    gen_ms = max_over_ranks(gen_tot / max(fills, 1), coll)
+    jump_ms = max_over_ranks(jump_tot / max(fills, 1), coll)
 
     # -- global checksum of one full 2^34 range (config 4 verification)
     g.seek(start)
@@ -643,6 +649,7 @@ def main():
         if int(ok.item()) == 0:
             e2e = {"unavailable": "no pinned host memory for the end-to-end buffer on some rank"}
         else:
+            g.set_prefetch(2)  # the public API's default positioning (co-resident prefetch)
             g.seek(rank * ew)
             g.fill_u32(host)  # warm-up
             g.skip(Te - ew)
