@@ -62,12 +62,6 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 #ifndef VMT_GEN_HIST
 #define VMT_GEN_HIST 1
 #endif
-// VMT_PAIR128=1: 16-byte output stores from 8-byte lane pairs via shuffles
-// (bit-exact; measured 4.22 vs 6.08 TB/s -- each predicated 128-bit store
-// leaves half of every quarter-warp idle, doubling the L1 wavefronts).
-#ifndef VMT_PAIR128
-#define VMT_PAIR128 0
-#endif
 
 template <int MODE>
 __host__ __device__ constexpr int elem_bytes() {
@@ -284,9 +278,6 @@ __device__ __forceinline__ void gen_window(std::uint32_t* ring, int base, int a,
         o = static_cast<E*>(out) + (MODE == MODE_F64_RES53 ? (rel >> 1) : rel);
     }
     std::uint32_t NW[STAGE ? R : 1][V];
-    // paired 16-byte stores: full windows of 32-bit words, 16-byte aligned rows (VEC)
-    constexpr bool kPair = VMT_PAIR128 && MODE == MODE_U32 && VEC && FULL && !STAGE && V == 2 && L >= 4;
-    std::uint32_t pend[2];
 #pragma unroll
     for (int i = 0; i < R; ++i) {
         std::uint32_t nw[V];
@@ -333,31 +324,6 @@ __device__ __forceinline__ void gen_window(std::uint32_t* ring, int base, int a,
 #pragma unroll
             for (int v = 0; v < V; ++v)
                 NW[i][v] = nw[v];
-        } else if (kPair) {
-            // 16-byte stores from 8-byte lane pairs: thread pairs (q, q^1) of
-            // a row swap halves of two consecutive rows with shuffles; the even
-            // thread stores row i-1's four lanes, the odd one row i's (a pure
-            // 64-bit store probe reaches 5.9 TB/s, a 128-bit one 6.5; this
-            // pairing is slower still, see VMT_PAIR128)
-            std::uint32_t tw[V];
-#pragma unroll
-            for (int v = 0; v < V; ++v)
-                tw[v] = temper(nw[v]);
-            if (i % 2 == 0 && i + 1 < R) {
-                pend[0] = tw[0];
-                pend[1] = tw[1];
-            } else if (i % 2 == 1) {
-                const std::uint32_t a0 = __shfl_xor_sync(0xFFFFFFFFu, tw[0], 1);
-                const std::uint32_t a1 = __shfl_xor_sync(0xFFFFFFFFu, tw[1], 1);
-                const std::uint32_t b0 = __shfl_xor_sync(0xFFFFFFFFu, pend[0], 1);
-                const std::uint32_t b1 = __shfl_xor_sync(0xFFFFFFFFu, pend[1], 1);
-                if (q & 1)
-                    store_out(reinterpret_cast<uint4*>(o + i * LT - 2), make_uint4(a0, a1, tw[0], tw[1]));
-                else
-                    store_out(reinterpret_cast<uint4*>(o + (i - 1) * LT), make_uint4(pend[0], pend[1], b0, b1));
-            } else { // the odd run's last row
-                store_out(reinterpret_cast<uint2*>(o + i * LT), make_uint2(tw[0], tw[1]));
-            }
         } else {
             std::uint32_t tw[V];
 #pragma unroll

@@ -10,7 +10,7 @@ $NV -DMB_VW=1 -o $D/_bin/mb_vw1 $D/mb_gen.cu
 $NV -DMB_VW=2 -DVMT_GEN_MINB=2 -o $D/_bin/mb_2cta $D/mb_gen.cu       # run with args: 20 296
 $NV -DMB_R=4 -DMB_VW=4 -DVMT_GEN_MINB=1 -o $D/_bin/mb_r4v4 $D/mb_gen.cu
 $NV -DMB_TMA=true -o $D/_bin/mb_tma208 $D/mb_gen.cu
-$NV -DVMT_PAIR128=1 -o $D/_bin/mb_pair128 $D/mb_gen.cu
+# (VMT_PAIR128, the shuffle-paired 128-bit stores of pair128.log, was removed from the kernel after it measured slower)
 $NV -DNC=256 -DCV=2 -o $D/_bin/ws_256 $D/ws_gen.cu
 $NV -o $D/_bin/probe_st $D/probe_st.cu
 $NV -o $D/_bin/pipes $D/pipes.cu                                      # pipe rates (pipes.log)
