@@ -19,3 +19,4 @@ $NV -DSV=2 -o $D/_bin/split_v2 $D/split_gen.cu                        # runs of 
 $NV -o $D/_bin/inplace $D/inplace_gen.cu                              # in-place ring, static slots
 $NV -o $D/_bin/probe_power $D/probe_power.cu                          # store paths: rate + power (power.sh)
 $NV -DSTAGE=1 -o $D/_bin/inplace_tma $D/inplace_gen.cu                  # + TMA bulk stores of double-buffered windows
+$NV -o $D/_bin/qmajor $D/qmajor_gen.cu                                # lane-pair-major ring, 128-bit ring accesses
