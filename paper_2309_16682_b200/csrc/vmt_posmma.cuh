@@ -39,7 +39,12 @@
 namespace vmt_b200 {
 
 constexpr int kPmM = 128;                  // lane states per tile
-constexpr int kPmNH = 208;                 // output bit columns per MMA (N)
+#ifndef VMT_POSMMA_NH
+#define VMT_POSMMA_NH 208
+#endif
+constexpr int kPmNH = VMT_POSMMA_NH;       // output bit columns per MMA (N); 2 x kPmNH must be whole state words
+static_assert((2 * VMT_POSMMA_NH) % 32 == 0 && (kN * 32) % (2 * VMT_POSMMA_NH) == 0 && VMT_POSMMA_NH % 16 == 0,
+              "tile = whole state words, tiling 19968 columns");
 constexpr int kPmN = 2 * kPmNH;            // per tile: two MMAs side by side in TMEM = 13 state words
 constexpr int kPmKE = 128;                 // K elements (input bits) per stage = 64 bytes of FP4
 constexpr int kPmStages = 3;
