@@ -639,7 +639,7 @@ cudaEvent_t* prof_next(vmt_generator* h) {
 // positioning is one FP4 GEMM (capi_gemmpos.inl, measured ~0.03 ms + 0.165 us
 // per lane state: 1024 rows 0.21 ms, 4736 rows 0.79 ms) rather than jumps.
 std::uint64_t plan_chunks(unsigned L, std::uint64_t n, std::uint64_t c_max, int sms, int mode = MODE_U32,
-                          bool gemm = false) {
+                          bool gemm = false, double lane_speed = 1.0) {
     const double per_jump = 0.43e-6 * 148.0 / (double)sms;
     auto t_jump = [&](double jobs) -> double {
         if (jobs <= 0)
@@ -651,7 +651,10 @@ std::uint64_t plan_chunks(unsigned L, std::uint64_t n, std::uint64_t c_max, int 
     // store modes saturate at ~1.6e12 4-byte elements/s per GPU; doubles (one
     // per word) at ~5.1e11/s (measured at L=8: 4.1 TB/s)
     const bool dbl = mode == MODE_F64 || mode == MODE_F64_REAL3;
-    const double r_lane = fused ? 5.5e8 : 3.2e8, peak_sm = (fused ? 3.4e12 : dbl ? 5.1e11 : 1.6e12) / 148.0;
+    // lane_speed: threads per lane of the kernel shape relative to the R=13,
+    // VW=2 shape the constants were measured with (VW=1 has twice as many)
+    const double r_lane = (fused ? 5.5e8 : 3.2e8) * lane_speed,
+                 peak_sm = (fused ? 3.4e12 : dbl ? 5.1e11 : 1.6e12) / 148.0;
     auto t_pos = [&](std::uint64_t C) -> double {
         const double rows = double(C) * L;
         if (gemm && rows >= (double)gemm_min_rows())
@@ -696,7 +699,15 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     // stored, so the 32-byte row segments of a lane group cost nothing), with
     // one wave of chunks (4 CTAs per SM)
     const bool xor_groups = h->variant == 0 && mode == MODE_XOR && h->L == 32;
-    const Variant& v = pick_variant(h->L, xor_groups ? 7 : h->variant);
+    // 8-lane store fills: one lane per thread (variant 4, 128 threads per
+    // chunk) instead of two (64 threads: 2 warps per chunk leave the SM
+    // latency-bound): 2^28 words per fill u32 0.48 -> 0.33 ms, f32 0.51-0.81
+    // -> 0.35, f64 0.62 -> 0.47 (profiles/r02_c2_variants.log). Two-word
+    // doubles (RES53) need two lanes per thread.
+    const bool l8_vw1 = h->variant == 0 && h->L == 8 &&
+                        (mode == MODE_U32 || mode == MODE_F32 || mode == MODE_F64 || mode == MODE_F64_REAL3);
+    const Variant& v = pick_variant(h->L, xor_groups ? 7 : l8_vw1 ? 4 : h->variant);
+    const double lane_speed = double(v.NT) / double(v.G) / 8.0;
     const int groups = v.L / v.G; // CTAs per chunk (lane groups)
     const std::uint64_t nb = b1 - b0;
     // VEC when the destination is aligned for the vector width: the element
@@ -730,7 +741,7 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     const bool gemm_plan = repeat && (mode != MODE_XOR || (h->gemm && h->gemm->last_valid && b0 > h->gemm->last_b0 &&
                                                            usable_base(*h->gemm, b0 - h->gemm->last_b0) != 0));
     std::uint64_t C = h->max_chunks ? std::min<std::uint64_t>(c_max, h->max_chunks)
-                                    : plan_chunks(h->L, n, c_max, sms, mode, gemm_plan);
+                                    : plan_chunks(h->L, n, c_max, sms, mode, gemm_plan, lane_speed);
     static const bool debug = std::getenv("VMT_DEBUG") != nullptr;
     if (debug)
         std::fprintf(stderr, "[vmt] L=%u R=%d NT=%d smem=%d occ=%d chunks=%llu blocks=%llu mode=%d vec=%d\n", h->L,
@@ -846,7 +857,7 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
                                                   : max_grid / groups),
             nbn);
         std::uint64_t Cn = h->max_chunks ? std::min<std::uint64_t>(c_max_n, h->max_chunks)
-                                         : plan_chunks(h->L, n, c_max_n, sms, mode, gemm_plan);
+                                         : plan_chunks(h->L, n, c_max_n, sms, mode, gemm_plan, lane_speed);
         const std::uint64_t Bn = (nbn + Cn - 1) / Cn;
         Cn = (nbn + Bn - 1) / Bn;
         prefetch_now = Cn == C && Bn == B && next_b0 >= b0;
