@@ -99,3 +99,22 @@ def test_lane_cross_correlation_matches_reference(golden):
         assert r.pass_ == c["pass"]
     with pytest.raises(V.InvalidArgument):
         V.lane_cross_correlation(V.VmtGenerator(1, V.VmtConfig(1)), 1000)
+
+
+@pytest.mark.parametrize("L", [8, 16, 32])
+def test_counts_long_chunks_match_stored_words(L):
+    """Long chunks (max_chunks=8 at 2^28 words: 6721 / 3360 / 1680 blocks per
+    chunk for L = 8 / 16 / 32, far past any 16-bit count): the fused counts
+    equal a byte histogram of the same stored words (torch.bincount on the
+    GPU), and the one-bit count their popcount."""
+    n = 1 << 28
+    a = V.VmtGenerator(77, V.VmtConfig(L))
+    a.set_tuning(max_chunks=8)
+    ones, bins = a.stat_counts(n)
+    b = V.VmtGenerator(77, V.VmtConfig(L))
+    out = torch.empty(n, dtype=torch.uint32, device="cuda")
+    b.fill_u32(out)
+    ref = torch.bincount(out.view(torch.uint8).to(torch.int64), minlength=256).cpu().numpy().astype(np.uint64)
+    assert np.array_equal(np.asarray(bins, np.uint64), ref)
+    assert ones == int((ref * POP8).sum())
+    assert int(ref.sum()) == 4 * n
