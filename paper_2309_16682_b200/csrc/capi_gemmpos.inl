@@ -265,9 +265,14 @@ bool gemm_position(vmt_generator* h, GemmPos& gp, const std::uint32_t* src, std:
     std::uint64_t base = usable_base(gp, delta);
     if (base == 0) {
         // no matrix yet: build it for the smallest recently seen delta in
-        // [delta-4, delta], so that the alternating neighbour reuses it
-        base = delta;
-        for (std::uint64_t k = 4; k >= 1; --k)
+        // [delta-4, delta], and at most delta-1: fills of n words alternate
+        // between block deltas floor(n/bw) and floor(n/bw)+1 in whichever
+        // order the first repeats come, and both must reuse this matrix (a
+        // second 200 MB build, ~8 ms, cost 2^26-word fills at L=32 4x their
+        // steady-state time: profiles/r02_plan_sweep.log); the block of
+        // in-place advance this adds to exact repeats costs microseconds
+        base = delta > 1 ? delta - 1 : delta;
+        for (std::uint64_t k = 4; k >= 2; --k)
             if (k < delta && gp.seen.count(delta - k)) {
                 base = delta - k;
                 break;
