@@ -90,13 +90,29 @@ except Exception:
     h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[2]))
 get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
 mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+FI = getattr(nv, "NVML_FI_DEV_POWER_INSTANT", None)
+
+
+def power():
+    # instantaneous board power when the driver offers it (nvmlDeviceGetPowerUsage
+    # is a ~1 s average and lags a 0.25 s timed region), else the average
+    if FI is not None:
+        try:
+            v = nv.nvmlDeviceGetFieldValues(h, [FI])[0]
+            if v.nvmlReturn == 0:
+                return v.value.uiVal / 1000.0
+        except Exception:
+            pass
+    return nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+
+
 print("ready", flush=True)
 i = 0
 while True:
     w = ""
     if i % 4 == 0:
         try:
-            w = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+            w = power()
         except Exception:
             pass
     i += 1
