@@ -18,12 +18,15 @@
 #include <cudaTypedefs.h>
 
 #ifndef VMT_GEMM_MIN_ROWS
-#define VMT_GEMM_MIN_ROWS 1024
+#define VMT_GEMM_MIN_ROWS 256
 #endif
 
 namespace {
 
-// below this many lane states the polynomial jumps win (env VMT_GEMM_MIN_ROWS overrides)
+// below this many lane states the polynomial jumps win (env VMT_GEMM_MIN_ROWS
+// overrides). 256 since round 2: our GEMM positions 592 lane states in ~0.1 ms
+// against ~0.25 ms of jumps (config 1 0.22 -> 0.20 ms per fill, 2^24-word
+// fills at L=16 0.20 -> 0.12 ms; profiles/r02_plan_sweep.log)
 inline std::uint64_t gemm_min_rows() {
     static const std::uint64_t v =
         std::getenv("VMT_GEMM_MIN_ROWS") ? std::strtoull(std::getenv("VMT_GEMM_MIN_ROWS"), nullptr, 10)

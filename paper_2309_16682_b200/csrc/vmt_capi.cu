@@ -638,6 +638,9 @@ cudaEvent_t* prof_next(vmt_generator* h) {
 // ~3.4e12 words/s per GPU; and when the previous fill had the same size the
 // positioning is one FP4 GEMM (capi_gemmpos.inl, measured ~0.03 ms + 0.165 us
 // per lane state: 1024 rows 0.21 ms, 4736 rows 0.79 ms) rather than jumps.
+#ifndef VMT_PLAN_RLANE
+#define VMT_PLAN_RLANE 3.2e8
+#endif
 std::uint64_t plan_chunks(unsigned L, std::uint64_t n, std::uint64_t c_max, int sms, int mode = MODE_U32,
                           bool gemm = false, double lane_speed = 1.0) {
     const double per_jump = 0.43e-6 * 148.0 / (double)sms;
@@ -653,7 +656,7 @@ std::uint64_t plan_chunks(unsigned L, std::uint64_t n, std::uint64_t c_max, int 
     const bool dbl = mode == MODE_F64 || mode == MODE_F64_REAL3;
     // lane_speed: threads per lane of the kernel shape relative to the R=13,
     // VW=2 shape the constants were measured with (VW=1 has twice as many)
-    const double r_lane = (fused ? 5.5e8 : 3.2e8) * lane_speed,
+    const double r_lane = (fused ? 5.5e8 : VMT_PLAN_RLANE) * lane_speed,
                  peak_sm = (fused ? 3.4e12 : dbl ? 5.1e11 : 1.6e12) / 148.0;
     auto t_pos = [&](std::uint64_t C) -> double {
         const double rows = double(C) * L;
