@@ -308,3 +308,30 @@ def test_tensor_core_prefetch_two_generators_interleaved():
         if i == 4:
             del tcs[1], refs[1]  # destroyed with its prefetch possibly in flight
     assert tcs[0].prefetch_stats()["used"] >= 3
+
+
+@pytest.mark.parametrize("L,chunks,n", [(16, 20, (1 << 24) + 33), (32, 9, 1 << 24), (16, 50, 1 << 26)])
+@pytest.mark.parametrize("prefetch", [0, 2])
+def test_gemm_positioning_small_row_counts(L, chunks, n, prefetch):
+    """The GEMM positions from 256 lane states since round 2 (320, 288 and 800
+    rows here, one to four pair tiles): serial and co-resident, every fill
+    word-identical to the polynomial-jump positioning."""
+    ref = V.VmtGenerator(99, V.VmtConfig(L))
+    ref.set_tuning(max_chunks=chunks)
+    ref.set_positioning(1)
+    ref.set_prefetch(0)
+    gem = V.VmtGenerator(99, V.VmtConfig(L))
+    gem.set_tuning(max_chunks=chunks)
+    gem.set_prefetch(prefetch)
+    a = torch.empty(n, dtype=torch.uint32, device="cuda")
+    b = torch.empty(n, dtype=torch.uint32, device="cuda")
+    for i in range(7):
+        ref.fill_u32(a)
+        gem.fill_u32(b)
+        torch.cuda.synchronize()
+        assert torch.equal(i32(a), i32(b)), (L, chunks, n, prefetch, i)
+    assert gem.positioning_stats()["cached_matrices"] >= 1
+    if prefetch:
+        assert gem.prefetch_stats()["used"] >= 2
+    else:
+        assert gem.positioning_stats()["gemm_positionings"] >= 2
