@@ -57,6 +57,13 @@ constexpr int kPmThreads = 192;
 constexpr int kPmSmem = kPmStages * kPmStageBytes + 1024 /* align */ + 128 /* barriers */;
 constexpr int kPmSfCol = 448;              // TMEM columns [448, 512): unit scale factors
 
+// Parity of an fp32 accumulator holding an exact integer sum v < 2^23: the
+// lowest mantissa bit of v + 2^23 (one FADD on the FMA pipe instead of an
+// F2I conversion on the slow pipe; 416 per epilogue thread and tile)
+__device__ __forceinline__ std::uint32_t parity_bit(std::uint32_t acc) {
+    return __float_as_uint(__uint_as_float(acc) + 8388608.0f) & 1u;
+}
+
 struct PosMmaParams {
     std::uint32_t* dst;       // [C][624][L] jumped by the matrix (the next fill's)
     int L;
@@ -252,7 +259,7 @@ __global__ void __launch_bounds__(kPmThreads, 1)
                 std::uint32_t w = 0;
 #pragma unroll
                 for (int b = 0; b < 32; ++b) // exact fp32 sums of 0/1 products: bit = parity
-                    w |= ((std::uint32_t)__float2int_rn(__uint_as_float(v[b])) & 1u) << b;
+                    w |= parity_bit(v[b]) << b;
                 const int k = n * (kPmN / 32) + j;
                 if (valid)
                     dst[(long long)k * p.L] = k == 0 ? (w & kUpperMask) : w;
@@ -469,7 +476,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPmThreads, 1)
                 std::uint32_t w = 0;
 #pragma unroll
                 for (int b = 0; b < 32; ++b)
-                    w |= ((std::uint32_t)__float2int_rn(__uint_as_float(v[b])) & 1u) << b;
+                    w |= parity_bit(v[b]) << b;
                 const int k = n * (kPmN / 32) + j;
                 if (valid)
                     dst[(long long)k * p.L] = k == 0 ? (w & kUpperMask) : w;
