@@ -1,4 +1,6 @@
-"""Fused XOR checksum of 2^34 words at L=32 (the bench's e2e_xor call) by
+"""(Experiment record: variant 9 was a temporary make_variant<32, 8, 13, 1>
+instantiation, removed after this measurement.)
+Fused XOR checksum of 2^34 words at L=32 (the bench's e2e_xor call) by
 kernel variant: 7 = 8-lane groups, two lanes per thread (the default for the
 fused mode); 9 = 8-lane groups, one lane per thread (twice the warps);
 0 = the store-mode default shape. ms per call (8 calls after 3 warm-up)."""
