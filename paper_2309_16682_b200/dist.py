@@ -42,9 +42,10 @@ def collective_device(device: torch.device | str | None = None) -> torch.device:
     return torch.device("cpu")
 
 
-def combine_xor(partial: int, device: torch.device | str | None = None) -> int:
-    """XOR of every rank's 32-bit partial (all-gather + local fold)."""
-    if not dist.is_initialized() or dist.get_world_size() == 1:
+def combine_xor(partial: int, device: torch.device | str | None = None, *, collective: bool = False) -> int:
+    """XOR of every rank's 32-bit partial (all-gather + local fold).
+    collective=True runs the all-gather even for a single rank (tests)."""
+    if not dist.is_initialized() or (dist.get_world_size() == 1 and not collective):
         return partial & 0xFFFFFFFF
     world = dist.get_world_size()
     device = collective_device(device)
@@ -54,8 +55,10 @@ def combine_xor(partial: int, device: torch.device | str | None = None) -> int:
     return fold_xor(int(o.item()) for o in out)
 
 
-def max_over_ranks(value: float, device: torch.device | str | None = None) -> float:
-    if not dist.is_initialized() or dist.get_world_size() == 1:
+def max_over_ranks(value: float, device: torch.device | str | None = None, *, collective: bool = False) -> float:
+    """Maximum over ranks (the bench's step time). collective=True runs the
+    all-reduce even for a single rank (tests)."""
+    if not dist.is_initialized() or (dist.get_world_size() == 1 and not collective):
         return value
     device = collective_device(device)
     t = torch.tensor([value], dtype=torch.float64, device=device)
