@@ -439,7 +439,7 @@ def extras(dev) -> dict:
                                   "roofline": {"bound": "alu", "limited_by": "integer ALU issue of the polynomial "
                                                "jump (p(F)s as a word convolution: ~19960 coefficient steps x 20 "
                                                "words x LOP3 per jump); see profiles/r02_summary.md"},
-                                  "note": "4 polynomial jumps per state from 12-bit digit tables (bits 16..63 of the 64-bit distance) + a direct advance by the low 16 bits"}
+                                  "note": "3 polynomial jumps per state from 16-bit digit tables (bits 16..63 of the 64-bit distance) + a direct advance by the low 16 bits"}
     # fused statistics consumer (monobit + chi2 byte histogram), 2^32 words, nothing stored
     n = 1 << 32
     g = V.VmtGenerator(5489, V.VmtConfig(32))
