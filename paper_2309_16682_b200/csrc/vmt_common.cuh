@@ -137,10 +137,23 @@ __device__ __forceinline__ std::uint32_t twist(std::uint32_t xk, std::uint32_t x
 // Tempering (mt19937.hpp:61-66; lane form lane_ops.hpp:88-93). Left shifts
 // are multiplies so they issue on the FMA pipe. (Right shifts as the high word
 // of IMAD.WIDE were measured 6% slower: the wide multiply is not FMA-pipe only.)
+#ifndef VMT_TEMPER_SHL_ALU
+#define VMT_TEMPER_SHL_ALU 0 // experiment: bit 0 / bit 1 = the << 7 / << 15 as ALU-pipe shifts
+#endif
+template <int S, bool ALU>
+__device__ __forceinline__ std::uint32_t shl(std::uint32_t x) {
+    if (ALU) {
+        std::uint32_t r;
+        // (ptxas turns a plain shl into IMAD.SHL; the funnel shift stays an SHF)
+        asm("shf.l.wrap.b32 %0, 0, %1, %2;" : "=r"(r) : "r"(x), "n"(S));
+        return r;
+    }
+    return mul_lo(x, 1u << S);
+}
 __device__ __forceinline__ std::uint32_t temper(std::uint32_t y) {
     y ^= shr<11, (VMT_SHR_FMA & 2) != 0>(y);
-    y = xor_and<0x9D2C5680u>(y, mul_lo(y, 1u << 7));
-    y = xor_and<0xEFC60000u>(y, mul_lo(y, 1u << 15));
+    y = xor_and<0x9D2C5680u>(y, shl<7, (VMT_TEMPER_SHL_ALU & 1) != 0>(y));
+    y = xor_and<0xEFC60000u>(y, shl<15, (VMT_TEMPER_SHL_ALU & 2) != 0>(y));
     return y ^ shr<18, (VMT_SHR_FMA & 4) != 0>(y);
 }
 
