@@ -100,17 +100,38 @@ int p2_stages_for(int smem_bytes) {
 
 bool posmma_run(GemmPos& gp, const CUtensorMap& tmap_b, const std::uint32_t* src, std::uint32_t* dst, unsigned L,
                 std::uint64_t rows, int sms, cudaStream_t st, unsigned nl, unsigned lane0,
-                int stages = kP2MaxStages);
+                int stages = kP2MaxStages, bool prepared = false);
 
+// Whether posmma_launch has a matrix (and its TMA descriptor) for this delta
+bool posmma_ready(GemmPos& gp, std::uint64_t delta) {
+    const bool pair = posmma_pair();
+    auto& maps = pair ? gp.tmaps2 : gp.tmaps;
+    return maps.find(delta) != maps.end() && gp.mats.count(delta) != 0;
+}
+
+// prepared: posmma_prepare has already written the states' FP4 operand
 bool posmma_launch(GemmPos& gp, std::uint64_t delta, const std::uint32_t* src, std::uint32_t* dst, unsigned L,
-                   std::uint64_t rows, int sms, cudaStream_t st, int stages = kP2MaxStages) {
+                   std::uint64_t rows, int sms, cudaStream_t st, int stages = kP2MaxStages, bool prepared = false) {
     const bool pair = posmma_pair();
     auto it = (pair ? gp.tmaps2 : gp.tmaps).find(delta);
     if (it == (pair ? gp.tmaps2 : gp.tmaps).end() || !gp.mats.count(delta))
         return false;
     gp.last_use[delta] = gp.tick;
-    return posmma_run(gp, it->second, src, dst, L, rows, sms, st, L, 0, stages);
+    return posmma_run(gp, it->second, src, dst, L, rows, sms, st, L, 0, stages, prepared);
 }
+
+#ifdef VMT_TIMELINE
+// experiments: per-CTA {start ns, end ns, SM id} of the last generation launch
+// ([0, 3072)) and the last positioning GEMM ([3072, 6144)); vmt_debug_timeline
+unsigned long long* timeline_buf() {
+    static unsigned long long* buf = nullptr;
+    if (!buf) {
+        VMT_CUDA(cudaMalloc(&buf, 6144 * sizeof(unsigned long long)));
+        VMT_CUDA(cudaMemset(buf, 0, 6144 * sizeof(unsigned long long)));
+    }
+    return buf;
+}
+#endif
 
 template <int S>
 void p2_launch(int grid, cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const PosMmaParams& pp) {
@@ -120,8 +141,37 @@ void p2_launch(int grid, cudaStream_t st, const CUtensorMap& a, const CUtensorMa
 // Lanes [lane0, lane0 + nl) of every state of dst (interleaved [.][624][L])
 // = lanes [0, nl) of src times the FP4 matrix behind tmap_b (nl = L, lane0 =
 // 0: every lane, chunk positioning).
+// The A operand of posmma_run: lanes [0, nl) of the `rows` lane states of src as
+// FP4 rows (zero-padded to whole tiles) in gp.pm_a, with its TMA descriptor.
+// The co-resident prefetch calls it on the fill's own stream BEFORE the
+// generation kernel: queued on the side stream, the conversion's many small
+// CTAs raced the generation kernel for the SMs and, when they won, the
+// generation CTAs were packed 3-4 per SM onto the first SMs that drained
+// (config 1: 0.20 ms per fill at 60 chunks but 0.32 ms at 48 / 64 / 80,
+// profiles/r02_summary.md).
+bool posmma_prepare(GemmPos& gp, const std::uint32_t* src, unsigned L, std::uint64_t rows, cudaStream_t st,
+                    unsigned nl) {
+    const std::uint64_t tile_rows = posmma_pair() ? 2 * kPmM : kPmM;
+    const std::uint64_t rows_pad = (rows + tile_rows - 1) / tile_rows * tile_rows;
+    gp.pm_a.reserve(rows_pad * kWB / 2);
+    if (gp.pm_tmap_ptr != gp.pm_a.p || gp.pm_tmap_rows != rows_pad) {
+        if (!make_tmap_fp4(gp.pm_tmap_a, gp.pm_a.p, rows_pad, kPmM))
+            return false;
+        gp.pm_tmap_ptr = gp.pm_a.p;
+        gp.pm_tmap_rows = rows_pad;
+    }
+    if (rows_pad > rows)
+        VMT_CUDA(cudaMemsetAsync(gp.pm_a.p + rows * kWB / 2, 0, (rows_pad - rows) * kWB / 2, st));
+    const long long nwords = (long long)rows * kN;
+    vmt_states_to_fp4_kernel<<<(unsigned)((nwords + 255) / 256), 256, 0, st>>>(
+        src, (int)L, 0, (int)nl, nwords, reinterpret_cast<std::uint8_t*>(gp.pm_a.p));
+    VMT_CUDA(cudaGetLastError());
+    return true;
+}
+
 bool posmma_run(GemmPos& gp, const CUtensorMap& tmap_b, const std::uint32_t* src, std::uint32_t* dst, unsigned L,
-                std::uint64_t rows, int sms, cudaStream_t st, unsigned nl, unsigned lane0, int stages) {
+                std::uint64_t rows, int sms, cudaStream_t st, unsigned nl, unsigned lane0, int stages,
+                bool prepared) {
     const bool pair = posmma_pair();
     {
         // function attributes are per device (vmt_multi_gpu_fill drives several)
@@ -149,20 +199,12 @@ bool posmma_run(GemmPos& gp, const CUtensorMap& tmap_b, const std::uint32_t* src
     }
     const std::uint64_t tile_rows = pair ? 2 * kPmM : kPmM;
     const std::uint64_t rows_pad = (rows + tile_rows - 1) / tile_rows * tile_rows;
-    gp.pm_a.reserve(rows_pad * kWB / 2);
-    if (gp.pm_tmap_ptr != gp.pm_a.p || gp.pm_tmap_rows != rows_pad) {
-        if (!make_tmap_fp4(gp.pm_tmap_a, gp.pm_a.p, rows_pad, kPmM))
-            return false;
-        gp.pm_tmap_ptr = gp.pm_a.p;
-        gp.pm_tmap_rows = rows_pad;
-    }
-    if (rows_pad > rows)
-        VMT_CUDA(cudaMemsetAsync(gp.pm_a.p + rows * kWB / 2, 0, (rows_pad - rows) * kWB / 2, st));
-    const long long nwords = (long long)rows * kN;
-    vmt_states_to_fp4_kernel<<<(unsigned)((nwords + 255) / 256), 256, 0, st>>>(
-        src, (int)L, 0, (int)nl, nwords, reinterpret_cast<std::uint8_t*>(gp.pm_a.p));
-    VMT_CUDA(cudaGetLastError());
+    if (!prepared && !posmma_prepare(gp, src, L, rows, st, nl))
+        return false;
     PosMmaParams pp;
+#ifdef VMT_TIMELINE
+    pp.tl = timeline_buf() + 3072;
+#endif
     pp.dst = dst;
     pp.L = (int)L;
     pp.rows = (int)rows;

@@ -835,8 +835,8 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     // -- predict the next fill (same size, same gap) and position its chunks
     // on the side stream while this fill's generation kernel runs: chunk c of
     // the next fill is chunk c of this one advanced by the same block delta
-    bool prefetch_now = false;
-    std::uint64_t next_b0 = 0;
+    bool prefetch_now = false, pref_prepared = false;
+    std::uint64_t next_b0 = 0, pref_base = 0;
     const std::uint64_t grid = C * groups;
     // the tensor-core form runs beside the generation kernel: only when that
     // kernel's CTAs spread evenly over the SMs (one wave) and leave room for
@@ -871,7 +871,21 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
             VMT_CUDA(cudaEventCreateWithFlags(&h->ev_chunks, cudaEventDisableTiming));
             VMT_CUDA(cudaEventCreateWithFlags(&h->ev_pref, cudaEventDisableTiming));
         }
-        VMT_CUDA(cudaEventRecord(h->ev_chunks, st));
+        // the tensor-core prefetch's FP4 state operand is written on this
+        // stream, ahead of the generation kernel (posmma_prepare)
+        if (tc_pref) {
+            try {
+                pref_base = usable_base(*h->gemm, next_b0 - b0);
+                pref_prepared = pref_base && posmma_ready(*h->gemm, pref_base) &&
+                                posmma_prepare(*h->gemm, h->chunks.p, h->L, C * h->L, st, h->L);
+            } catch (const VmtError&) { // e.g. no memory for the operand: generate without prefetching
+                cudaGetLastError();
+                h->prefetch = VMT_PREFETCH_OFF;
+                prefetch_now = false;
+            }
+        }
+        if (prefetch_now)
+            VMT_CUDA(cudaEventRecord(h->ev_chunks, st));
     }
     if (pe)
         VMT_CUDA(cudaEventRecord(pe[1], st));
@@ -893,6 +907,9 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     p.out_chunk_stride = 0;
     p.blocks_per_chunk = (unsigned)B;
     p.lanes = h->L;
+#ifdef VMT_TIMELINE
+    p.tl = timeline_buf();
+#endif
     // Everything of the prefetch that can free device memory (growing the
     // alternate chunk buffer, evicting a cached skip polynomial: cudaFree
     // waits for the whole device) happens before the generation kernel is
@@ -920,9 +937,9 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
             VMT_CUDA(cudaStreamWaitEvent(h->side, h->ev_chunks, 0));
             // a cached matrix for the delta or for a base at most 4 blocks below
             // it (the rest regenerated in place, as in gemm_position)
-            const std::uint64_t delta = next_b0 - b0, base = usable_base(*h->gemm, delta);
-            if (base && posmma_launch(*h->gemm, base, h->chunks.p, h->chunks_alt.p, h->L, C * h->L, sms, h->side,
-                                      pref_stages)) {
+            const std::uint64_t delta = next_b0 - b0, base = pref_base;
+            if (pref_prepared && posmma_launch(*h->gemm, base, h->chunks.p, h->chunks_alt.p, h->L, C * h->L, sms,
+                                               h->side, pref_stages, true)) {
                 if (delta > base) {
                     vmt_advance_blocks_kernel<<<(unsigned)((C * h->L + kAdvWarps - 1) / kAdvWarps), 32 * kAdvWarps,
                                                 0, h->side>>>(h->chunks_alt.p, (int)h->L, (long long)(C * h->L),
@@ -1780,3 +1797,15 @@ int vmt_version(void) { return 100; }
 
 // Generator batches (config 3) and the single-process multi-GPU fill (config 4).
 #include "capi_batch.inl"
+
+#ifdef VMT_TIMELINE
+// experiments (profiles/scripts/timeline.py): copies the 6144-word timeline buffer to the host
+extern "C" int vmt_debug_timeline(unsigned long long* host_out) {
+    if (cudaDeviceSynchronize() != cudaSuccess)
+        return -1;
+    return cudaMemcpy(host_out, timeline_buf(), 6144 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) ==
+                   cudaSuccess
+               ? 0
+               : -1;
+}
+#endif

@@ -64,7 +64,23 @@ struct GenParams {
     unsigned long long out_chunk_stride; // batch mode: elements between chunks' outputs (0 = single stream)
     unsigned int blocks_per_chunk;
     unsigned int lanes;
+#ifdef VMT_TIMELINE
+    unsigned long long* tl; // experiments: per-CTA {start ns, end ns, SM id} (profiles/scripts/timeline.py)
+#endif
 };
+
+#ifdef VMT_TIMELINE
+__device__ __forceinline__ unsigned long long tl_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned tl_smid() {
+    unsigned s;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+    return s;
+}
+#endif
 
 // ---- per-word arithmetic (hand-scheduled LOP3 forms; SASS: 3 ALU + 2 FMA-pipe
 // ops for the twist, 6 ALU + 2 FMA-pipe ops for the temper) -----------------

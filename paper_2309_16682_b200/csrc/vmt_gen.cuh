@@ -482,6 +482,12 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::template lb_thread
     const unsigned chunk = blockIdx.x / kGroups;
     const int col0 = (int)(blockIdx.x % kGroups) * L; // first stream lane of this CTA
     const int tid = threadIdx.x;
+#ifdef VMT_TIMELINE
+    if (p.tl && tid == 0 && blockIdx.x < 1024) {
+        p.tl[blockIdx.x * 3] = tl_now();
+        p.tl[blockIdx.x * 3 + 2] = tl_smid();
+    }
+#endif
     const int q = tid % S::Q;   // vector column (lanes q*V .. q*V+V-1)
     const int rho = tid / S::Q; // run index within a window
 
@@ -711,6 +717,10 @@ __global__ void __launch_bounds__(GenShape<L, R, VW, W, TMA>::template lb_thread
         if (tid == 0)
             dst[0] = ones_red;
     }
+#ifdef VMT_TIMELINE
+    if (p.tl && tid == 0 && blockIdx.x < 1024)
+        p.tl[blockIdx.x * 3 + 1] = tl_now();
+#endif
 }
 
 } // namespace vmt_b200

@@ -70,6 +70,9 @@ struct PosMmaParams {
     int rows;                 // C * nl
     int m_tiles;              // ceil(rows / 128) (pair kernel: ceil(rows / 256))
     int nl, lane0;            // row r -> state r / nl, lane lane0 + r % nl (all lanes: nl = L, lane0 = 0)
+#ifdef VMT_TIMELINE
+    unsigned long long* tl;   // experiments: per-CTA {start ns, end ns, SM id}
+#endif
 };
 
 // ---- tcgen05 / TMA primitives -------------------------------------------------
@@ -361,6 +364,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPmThreads, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned rank = cluster_rank();
     const bool leader = rank == 0;
+#ifdef VMT_TIMELINE
+    if (p.tl && threadIdx.x == 0 && blockIdx.x < 1024) {
+        p.tl[blockIdx.x * 3] = tl_now();
+        p.tl[blockIdx.x * 3 + 2] = tl_smid();
+    }
+#endif
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);  // leader: its producer's expect_tx for both CTAs' bytes
@@ -488,6 +497,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPmThreads, 1)
                              : "memory");
         }
     }
+#ifdef VMT_TIMELINE
+    if (p.tl && threadIdx.x == 64 && blockIdx.x < 1024) // an epilogue warp: after its last tile
+        p.tl[blockIdx.x * 3 + 1] = tl_now();
+#endif
     tc_fence_before();
     cluster_sync_all();
     if (warp == 1) {
