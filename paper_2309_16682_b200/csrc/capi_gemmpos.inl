@@ -45,6 +45,7 @@ struct GemmPos {
     std::map<std::uint64_t, CUtensorMap> tmaps;
     std::map<std::uint64_t, CUtensorMap> tmaps2; // 104-row boxes for the CTA-pair kernel
     DevBuf<std::int8_t> pm_a; // FP4 state operand
+    DevBuf<unsigned> pm_ctr;  // tile counter of the pair kernel's scheduler (vmt_posmma.cuh)
     CUtensorMap pm_tmap_a;
     const void* pm_tmap_ptr = nullptr;
     std::uint64_t pm_tmap_rows = 0;
@@ -205,6 +206,11 @@ bool posmma_run(GemmPos& gp, const CUtensorMap& tmap_b, const std::uint32_t* src
 #ifdef VMT_TIMELINE
     pp.tl = timeline_buf() + 3072;
 #endif
+    if (!gp.pm_ctr.p) { // the pair kernel's tile counter: zero here, re-zeroed by every launch
+        gp.pm_ctr.reserve(1);
+        VMT_CUDA(cudaMemsetAsync(gp.pm_ctr.p, 0, sizeof(unsigned), st));
+    }
+    pp.tile_ctr = gp.pm_ctr.p;
     pp.dst = dst;
     pp.L = (int)L;
     pp.rows = (int)rows;

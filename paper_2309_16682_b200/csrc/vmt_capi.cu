@@ -15,6 +15,7 @@
 #include <list>
 #include <map>
 #include <memory>
+#include <cmath>
 #include <mutex>
 #include <set>
 #include <stdexcept>
@@ -625,24 +626,33 @@ cudaEvent_t* prof_next(vmt_generator* h) {
 }
 
 // Chunk count for a fill of n words: every chunk but the first costs L lane
-// jumps (positioning), every chunk adds generation parallelism. Minimise
-//   t(C) = t_jump((C-1) L) + (n / C) / min(L * r_lane, peak_sm / k),
-// k = ceil(C / sms) chunks sharing the busiest SM, with constants measured on
-// B200: a lane jump costs 0.43 us of whole-GPU
-// throughput with a latency floor of 0.16-0.5 ms, one lane generates ~3.2e8
-// words/s, an SM's store path saturates at ~1.6e12 / 148 words/s. Past one
-// chunk per SM only whole waves (multiples of sms) are candidates: a partial
-// wave leaves the SMs with one chunk more as the tail.
-//
+// jumps (positioning), every chunk adds generation parallelism. Minimise a
+// cost model t(C) with constants measured on B200 (DESIGN.md section 5,
+// profiles/r02_chunk_curve*.log):
+//  * generation: (n / C) / min(L r_lane, peak_sm / k), k = ceil(C / sms) chunks
+//    sharing the busiest SM; one lane of the R=13, VW=2 shape generates
+//    ~5.5e8 words/s (8.8e8 with one lane per thread), an SM's store path
+//    saturates at ~1.6e12 / 148 words/s. Past one chunk per SM only whole
+//    waves (multiples of sms) are candidates.
+//  * positioning by polynomial jumps (a fill shape seen for the first time):
+//    0.43 us of whole-GPU throughput per lane jump, latency floor 0.16-0.5 ms.
+//  * positioning by the FP4 GEMM (the previous fill had the same size):
+//    ~0.03 ms + 47 us per 256-state x 416-column tile and SM pair, in whole
+//    rounds of sms/2 tiles when it runs alone (1024 rows 0.17 ms, 4736 rows
+//    0.65 ms).
+//  * `overlap`: that GEMM will run beside the generation kernel as the
+//    tensor-core prefetch of the next fill. One chunk per SM: the two share
+//    the SMs' shared-memory bandwidth, measured t = max(t_gen + 0.5 t_pos,
+//    t_pos + 0.4 t_gen) with the tiles handed out dynamically (no whole
+//    rounds; 15% slower beside the 86 KB L=32 CTA, whose neighbour gets a
+//    shallower operand ring). More chunks per SM: t_gen + 0.75 t_pos.
 // Fused XOR fills (no stores) run at ~5.5e8 words/s per lane and saturate at
-// ~3.4e12 words/s per GPU; and when the previous fill had the same size the
-// positioning is one FP4 GEMM (capi_gemmpos.inl, measured ~0.03 ms + 0.165 us
-// per lane state: 1024 rows 0.21 ms, 4736 rows 0.79 ms) rather than jumps.
+// ~3.4e12 words/s per GPU.
 #ifndef VMT_PLAN_RLANE
-#define VMT_PLAN_RLANE 3.2e8
+#define VMT_PLAN_RLANE 5.5e8
 #endif
 std::uint64_t plan_chunks(unsigned L, std::uint64_t n, std::uint64_t c_max, int sms, int mode = MODE_U32,
-                          bool gemm = false, double lane_speed = 1.0) {
+                          bool gemm = false, double lane_speed = 1.0, bool overlap = false) {
     const double per_jump = 0.43e-6 * 148.0 / (double)sms;
     auto t_jump = [&](double jobs) -> double {
         if (jobs <= 0)
@@ -655,18 +665,27 @@ std::uint64_t plan_chunks(unsigned L, std::uint64_t n, std::uint64_t c_max, int 
     // per word) at ~5.1e11/s (measured at L=8: 4.1 TB/s)
     const bool dbl = mode == MODE_F64 || mode == MODE_F64_REAL3;
     // lane_speed: threads per lane of the kernel shape relative to the R=13,
-    // VW=2 shape the constants were measured with (VW=1 has twice as many)
-    const double r_lane = (fused ? 5.5e8 : VMT_PLAN_RLANE) * lane_speed,
+    // VW=2 shape (VW=1 has twice as many and runs a lane 1.6x as fast)
+    const double r_lane = fused ? 5.5e8 * lane_speed : VMT_PLAN_RLANE * (1.0 + 0.6 * (std::min(lane_speed, 2.0) - 1.0)),
                  peak_sm = (fused ? 3.4e12 : dbl ? 5.1e11 : 1.6e12) / 148.0;
-    auto t_pos = [&](std::uint64_t C) -> double {
+    const double pairs = std::max(1, sms / 2);
+    auto gemm_tiles = [&](std::uint64_t C) { return std::ceil(double(C) * L / 256.0) * 48.0; };
+    auto t_pos = [&](std::uint64_t C) -> double { // serial positioning
         const double rows = double(C) * L;
         if (gemm && rows >= (double)gemm_min_rows())
-            return std::min(t_jump(double(C - 1) * L), 0.03e-3 + rows * 1.65e-7 * 148.0 / (double)sms);
+            return std::min(t_jump(double(C - 1) * L), 0.03e-3 + std::ceil(gemm_tiles(C) / pairs) * 47e-6);
         return t_jump(double(C - 1) * L);
     };
     auto t = [&](std::uint64_t C) {
         const double k = (double)((C + sms - 1) / sms);
-        return t_pos(C) + (double(n) / double(C)) / std::min(L * r_lane, peak_sm / k);
+        const double t_gen = (double(n) / double(C)) / std::min(L * r_lane, peak_sm / k);
+        if (overlap && gemm && double(C) * L >= (double)gemm_min_rows()) {
+            if (k > 1)
+                return t_gen + 0.75 * t_pos(C);
+            const double tp = (0.03e-3 + gemm_tiles(C) / pairs * 47e-6) * (L == 32 ? 1.15 : 1.0);
+            return std::max(t_gen + 0.5 * tp, tp + 0.4 * t_gen);
+        }
+        return t_pos(C) + t_gen;
     };
     std::uint64_t best = 1;
     double tb = t(1);
@@ -743,8 +762,11 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     const bool repeat = h->positioning != 1 && h->last_fill_n == n;
     const bool gemm_plan = repeat && (mode != MODE_XOR || (h->gemm && h->gemm->last_valid && b0 > h->gemm->last_b0 &&
                                                            usable_base(*h->gemm, b0 - h->gemm->last_b0) != 0));
+    // the GEMM of the next fill will run beside this fill's generation kernel
+    const bool overlap_plan = gemm_plan && h->prefetch == VMT_PREFETCH_TENSOR && mode != MODE_XOR &&
+                              n >= kPrefetchMinWords;
     std::uint64_t C = h->max_chunks ? std::min<std::uint64_t>(c_max, h->max_chunks)
-                                    : plan_chunks(h->L, n, c_max, sms, mode, gemm_plan, lane_speed);
+                                    : plan_chunks(h->L, n, c_max, sms, mode, gemm_plan, lane_speed, overlap_plan);
     static const bool debug = std::getenv("VMT_DEBUG") != nullptr;
     if (debug)
         std::fprintf(stderr, "[vmt] L=%u R=%d NT=%d smem=%d occ=%d chunks=%llu blocks=%llu mode=%d vec=%d\n", h->L,
@@ -860,7 +882,7 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
                                                   : max_grid / groups),
             nbn);
         std::uint64_t Cn = h->max_chunks ? std::min<std::uint64_t>(c_max_n, h->max_chunks)
-                                         : plan_chunks(h->L, n, c_max_n, sms, mode, gemm_plan, lane_speed);
+                                         : plan_chunks(h->L, n, c_max_n, sms, mode, gemm_plan, lane_speed, overlap_plan);
         const std::uint64_t Bn = (nbn + Cn - 1) / Cn;
         Cn = (nbn + Bn - 1) / Bn;
         prefetch_now = Cn == C && Bn == B && next_b0 >= b0;

@@ -70,6 +70,7 @@ struct PosMmaParams {
     int rows;                 // C * nl
     int m_tiles;              // ceil(rows / 128) (pair kernel: ceil(rows / 256))
     int nl, lane0;            // row r -> state r / nl, lane lane0 + r % nl (all lanes: nl = L, lane0 = 0)
+    unsigned* tile_ctr;       // pair kernel: the launch's tile counter (zero before and after every launch)
 #ifdef VMT_TIMELINE
     unsigned long long* tl;   // experiments: per-CTA {start ns, end ns, SM id}
 #endif
@@ -299,7 +300,7 @@ constexpr int kP2StageBytes = kPmABytes + 2 * kP2BQBytes; // 21504
 // rings, which hide more of the TMA latency of the B operand (200 MB, streamed
 // from HBM: it does not fit in L2).
 constexpr int kP2Stages = 4;
-__host__ __device__ constexpr int p2_smem(int stages) { return stages * kP2StageBytes + 1024 + 128; }
+__host__ __device__ constexpr int p2_smem(int stages) { return stages * kP2StageBytes + 1024 + 256; }
 constexpr int kP2Smem = p2_smem(kP2Stages);
 // kind::mxf4, M = 256 (pair), N = 208
 constexpr unsigned kP2Idesc = (1u << 7) | (1u << 10) | ((unsigned)(kPmNH >> 3) << 17) | (1u << 23) |
@@ -347,6 +348,34 @@ __device__ __forceinline__ void tc_mma_mxf4_pair(unsigned tmem_d, unsigned long 
         : "memory");
 }
 
+// Tile scheduler of the pair kernel: the leader CTA's producer thread takes the
+// next tile from a global counter and publishes it to both CTAs of the pair
+// (a 4-slot ring per CTA, one mbarrier per slot), so a pair slowed by the
+// generation CTAs it shares its SMs with takes fewer tiles than a pair on free
+// SMs (config 1: 60-75 generation CTAs on 148 SMs). Consecutive tiles share
+// their N slice, so the pairs running together still share B through L2.
+// Every role reads the same sequence; a slot is rewritten four fetches later,
+// by which time the producer has loaded three more whole tiles, i.e. the MMA
+// thread is in tile i+3 and both epilogues are done with tile i+2.
+constexpr int kP2TileSlots = 4;
+__device__ __forceinline__ void mbar_wait_parity_cluster(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred done;\n"
+        "VMT_WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 done, [%0], %1;\n\t"
+        "@!done bra VMT_WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(unsigned bar_cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
+}
+// the seq-th tile of this pair (every thread of every role calls it with the same seq order)
+__device__ __forceinline__ int p2_next_tile(unsigned long long* tfull, const volatile unsigned* tslot, unsigned seq) {
+    mbar_wait_parity_cluster(&tfull[seq % kP2TileSlots], (seq / kP2TileSlots) & 1);
+    return (int)tslot[seq % kP2TileSlots];
+}
+
 // p.m_tiles = ceil(rows / 256) pair tiles; tmap_b boxes are 104 rows
 template <int kStages>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPmThreads, 1)
@@ -359,7 +388,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPmThreads, 1)
     unsigned long long* empty = full + kStages;
     unsigned long long* accf = empty + kStages; // MMA -> epilogues (both CTAs)
     unsigned long long* accd = accf + 1;           // epilogues (both CTAs) -> leader's MMA thread
-    unsigned* tmem_slot = reinterpret_cast<unsigned*>(accd + 1);
+    unsigned long long* tfull = accd + 1;          // leader's producer -> every role of both CTAs: tile published
+    unsigned* tslot = reinterpret_cast<unsigned*>(tfull + kP2TileSlots);
+    unsigned* tmem_slot = tslot + kP2TileSlots;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned rank = cluster_rank();
@@ -377,6 +408,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPmThreads, 1)
         }
         mbar_init(accf, 1);
         mbar_init(accd, 8); // 4 epilogue warps x 2 CTAs
+        for (int i = 0; i < kP2TileSlots; ++i)
+            mbar_init(&tfull[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&tmap_a)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&tmap_b)) : "memory");
@@ -405,13 +438,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPmThreads, 1)
     cluster_sync_all();
     tc_fence_after();
 
-    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int npairs = gridDim.x >> 1;
     const int ntiles = p.m_tiles * kPmNTiles;
     if (warp == 0) {
         if (lane == 0) {
             const unsigned long long pol = l2_policy_evict_last();
             unsigned it = 0;
-            for (int tile = pair; tile < ntiles; tile += npairs) {
+            for (unsigned seq = 0;; ++seq) {
+                int tile;
+                if (leader) {
+                    const unsigned t = atomicAdd(p.tile_ctr, 1u);
+                    const unsigned sl = seq % kP2TileSlots;
+                    tslot[sl] = t;
+                    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(map_to_rank(&tslot[sl], 1)), "r"(t)
+                                 : "memory");
+                    mbar_arrive_cluster(map_to_rank(&tfull[sl], 0));
+                    mbar_arrive_cluster(map_to_rank(&tfull[sl], 1));
+                    // every pair draws exactly one tile >= ntiles: the last of them re-zeroes the counter
+                    if (t == (unsigned)(ntiles + npairs - 1))
+                        atomicExch(p.tile_ctr, 0u);
+                    tile = (int)t;
+                } else
+                    tile = p2_next_tile(tfull, tslot, seq);
+                if (tile >= ntiles)
+                    break;
                 const int n = tile / p.m_tiles, m = tile % p.m_tiles;
                 for (int ks = 0; ks < kPmKSteps; ++ks, ++it) {
                     const int s = it % kStages;
@@ -433,7 +483,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPmThreads, 1)
     } else if (warp == 1) {
         if (leader && lane == 0) {
             unsigned it = 0, tcount = 0;
-            for (int tile = pair; tile < ntiles; tile += npairs, ++tcount) {
+            for (;; ++tcount) {
+                if (p2_next_tile(tfull, tslot, tcount) >= ntiles)
+                    break;
                 if (tcount > 0) { // both CTAs' epilogues have read the previous accumulators
                     mbar_wait_parity(accd, (tcount - 1) & 1);
                     tc_fence_after();
@@ -461,7 +513,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPmThreads, 1)
         const int r = (int)rank * kPmM + rq + lane; // row within the 256-row pair tile
         const unsigned accd_leader = map_to_rank(accd, 0);
         unsigned tcount = 0;
-        for (int tile = pair; tile < ntiles; tile += npairs, ++tcount) {
+        for (;; ++tcount) {
+            const int tile = p2_next_tile(tfull, tslot, tcount);
+            if (tile >= ntiles)
+                break;
             const int n = tile / p.m_tiles, m = tile % p.m_tiles;
             const int row = m * 2 * kPmM + r;
             const bool valid = row < p.rows;
