@@ -101,7 +101,7 @@ int p2_stages_for(int smem_bytes) {
 
 bool posmma_run(GemmPos& gp, const CUtensorMap& tmap_b, const std::uint32_t* src, std::uint32_t* dst, unsigned L,
                 std::uint64_t rows, int sms, cudaStream_t st, unsigned nl, unsigned lane0,
-                int stages = kP2MaxStages, bool prepared = false);
+                int stages = kP2MaxStages, bool prepared = false, bool dynamic_tiles = true);
 
 // Whether posmma_launch has a matrix (and its TMA descriptor) for this delta
 bool posmma_ready(GemmPos& gp, std::uint64_t delta) {
@@ -112,13 +112,14 @@ bool posmma_ready(GemmPos& gp, std::uint64_t delta) {
 
 // prepared: posmma_prepare has already written the states' FP4 operand
 bool posmma_launch(GemmPos& gp, std::uint64_t delta, const std::uint32_t* src, std::uint32_t* dst, unsigned L,
-                   std::uint64_t rows, int sms, cudaStream_t st, int stages = kP2MaxStages, bool prepared = false) {
+                   std::uint64_t rows, int sms, cudaStream_t st, int stages = kP2MaxStages, bool prepared = false,
+                   bool dynamic_tiles = true) {
     const bool pair = posmma_pair();
     auto it = (pair ? gp.tmaps2 : gp.tmaps).find(delta);
     if (it == (pair ? gp.tmaps2 : gp.tmaps).end() || !gp.mats.count(delta))
         return false;
     gp.last_use[delta] = gp.tick;
-    return posmma_run(gp, it->second, src, dst, L, rows, sms, st, L, 0, stages, prepared);
+    return posmma_run(gp, it->second, src, dst, L, rows, sms, st, L, 0, stages, prepared, dynamic_tiles);
 }
 
 #ifdef VMT_TIMELINE
@@ -172,7 +173,7 @@ bool posmma_prepare(GemmPos& gp, const std::uint32_t* src, unsigned L, std::uint
 
 bool posmma_run(GemmPos& gp, const CUtensorMap& tmap_b, const std::uint32_t* src, std::uint32_t* dst, unsigned L,
                 std::uint64_t rows, int sms, cudaStream_t st, unsigned nl, unsigned lane0, int stages,
-                bool prepared) {
+                bool prepared, bool dynamic_tiles) {
     const bool pair = posmma_pair();
     {
         // function attributes are per device (vmt_multi_gpu_fill drives several)
@@ -210,7 +211,9 @@ bool posmma_run(GemmPos& gp, const CUtensorMap& tmap_b, const std::uint32_t* src
         gp.pm_ctr.reserve(1);
         VMT_CUDA(cudaMemsetAsync(gp.pm_ctr.p, 0, sizeof(unsigned), st));
     }
-    pp.tile_ctr = gp.pm_ctr.p;
+    static const int tile_mode = std::getenv("VMT_POSMMA_TILES") ? std::atoi(std::getenv("VMT_POSMMA_TILES")) : 0;
+    // tiles from the counter unless the caller knows every pair is equally loaded
+    pp.tile_ctr = (tile_mode == 1 || (tile_mode == 0 && dynamic_tiles)) ? gp.pm_ctr.p : nullptr;
     pp.dst = dst;
     pp.L = (int)L;
     pp.rows = (int)rows;

@@ -857,7 +857,7 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
     // -- predict the next fill (same size, same gap) and position its chunks
     // on the side stream while this fill's generation kernel runs: chunk c of
     // the next fill is chunk c of this one advanced by the same block delta
-    bool prefetch_now = false, pref_prepared = false;
+    bool prefetch_now = false, pref_prepared = false, pref_ready = false;
     std::uint64_t next_b0 = 0, pref_base = 0;
     const std::uint64_t grid = C * groups;
     // the tensor-core form runs beside the generation kernel: only when that
@@ -898,8 +898,12 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
         if (tc_pref) {
             try {
                 pref_base = usable_base(*h->gemm, next_b0 - b0);
-                pref_prepared = pref_base && posmma_ready(*h->gemm, pref_base) &&
-                                posmma_prepare(*h->gemm, h->chunks.p, h->L, C * h->L, st, h->L);
+                pref_ready = pref_base && posmma_ready(*h->gemm, pref_base);
+                // (a generation kernel with one CTA per SM by occupancy cannot be
+                // packed; its operand is written on the side stream, in parallel)
+                static const int prep_mode = std::getenv("VMT_PREP_AHEAD") ? std::atoi(std::getenv("VMT_PREP_AHEAD")) : 0;
+                if (pref_ready && (prep_mode == 1 || (prep_mode == 0 && occ > 1)))
+                    pref_prepared = posmma_prepare(*h->gemm, h->chunks.p, h->L, C * h->L, st, h->L);
             } catch (const VmtError&) { // e.g. no memory for the operand: generate without prefetching
                 cudaGetLastError();
                 h->prefetch = VMT_PREFETCH_OFF;
@@ -960,8 +964,9 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
             // a cached matrix for the delta or for a base at most 4 blocks below
             // it (the rest regenerated in place, as in gemm_position)
             const std::uint64_t delta = next_b0 - b0, base = pref_base;
-            if (pref_prepared && posmma_launch(*h->gemm, base, h->chunks.p, h->chunks_alt.p, h->L, C * h->L, sms,
-                                               h->side, pref_stages, true)) {
+            // tiles handed out dynamically when the generation CTAs leave some SMs free
+            if (pref_ready && posmma_launch(*h->gemm, base, h->chunks.p, h->chunks_alt.p, h->L, C * h->L, sms,
+                                            h->side, pref_stages, pref_prepared, grid < (std::uint64_t)sms)) {
                 if (delta > base) {
                     vmt_advance_blocks_kernel<<<(unsigned)((C * h->L + kAdvWarps - 1) / kAdvWarps), 32 * kAdvWarps,
                                                 0, h->side>>>(h->chunks_alt.p, (int)h->L, (long long)(C * h->L),

@@ -447,7 +447,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPmThreads, 1)
             for (unsigned seq = 0;; ++seq) {
                 int tile;
                 if (leader) {
-                    const unsigned t = atomicAdd(p.tile_ctr, 1u);
+                    // no counter: the static round-robin (every pair equally loaded)
+                    const unsigned t = p.tile_ctr ? atomicAdd(p.tile_ctr, 1u)
+                                                  : (unsigned)(blockIdx.x >> 1) + seq * (unsigned)npairs;
                     const unsigned sl = seq % kP2TileSlots;
                     tslot[sl] = t;
                     asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(map_to_rank(&tslot[sl], 1)), "r"(t)
@@ -455,7 +457,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPmThreads, 1)
                     mbar_arrive_cluster(map_to_rank(&tfull[sl], 0));
                     mbar_arrive_cluster(map_to_rank(&tfull[sl], 1));
                     // every pair draws exactly one tile >= ntiles: the last of them re-zeroes the counter
-                    if (t == (unsigned)(ntiles + npairs - 1))
+                    if (p.tile_ctr && t == (unsigned)(ntiles + npairs - 1))
                         atomicExch(p.tile_ctr, 0u);
                     tile = (int)t;
                 } else
