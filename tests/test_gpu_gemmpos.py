@@ -119,6 +119,42 @@ print("ok")
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
+@pytest.mark.parametrize("tiles,prep", [("1", "1"), ("2", "2"), ("1", "2"), ("2", "1")])
+def test_tile_scheduler_and_operand_modes(tiles, prep):
+    """The pair kernel's tile order (VMT_POSMMA_TILES: 1 = from the global
+    counter, 2 = static round-robin) and the stream its FP4 operand is written
+    on (VMT_PREP_AHEAD: 1 = ahead of the generation kernel, 2 = side stream)
+    never change a word: co-resident prefetch with fewer chunks than SMs, one
+    chunk per SM, ragged fill sizes and a serial GEMM, against the polynomial
+    jumps."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, torch
+sys.path.insert(0, ".")
+import paper_2309_16682_b200 as V
+for L, n, chunks in ((16, (1 << 25) + 4097, 60), (16, 1 << 26, 148), (32, (1 << 26) + 33, 37), (8, 1 << 26, 100)):
+    ref = V.VmtGenerator(11, V.VmtConfig(L)); pre = V.VmtGenerator(11, V.VmtConfig(L)); ser = V.VmtGenerator(11, V.VmtConfig(L))
+    for g in (ref, pre, ser): g.set_tuning(max_chunks=chunks)
+    ref.set_positioning(1); ref.set_prefetch(0)
+    pre.set_prefetch(2)
+    ser.set_positioning(2); ser.set_prefetch(0)
+    a = torch.empty(n, dtype=torch.uint32, device="cuda"); b = torch.empty_like(a); c = torch.empty_like(a)
+    for i in range(7):
+        ref.fill_u32(a); pre.fill_u32(b); ser.fill_u32(c); torch.cuda.synchronize()
+        assert torch.equal(a.view(torch.int32), b.view(torch.int32)), (L, chunks, i, "prefetch")
+        assert torch.equal(a.view(torch.int32), c.view(torch.int32)), (L, chunks, i, "serial")
+    assert pre.prefetch_stats()["used"] >= 3, (L, chunks, pre.prefetch_stats())
+    assert ser.positioning_stats()["gemm_positionings"] >= 3
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, VMT_POSMMA_TILES=tiles, VMT_PREP_AHEAD=prep))
+    assert r.returncode == 0 and "ok" in r.stdout, (r.stdout[-500:], r.stderr[-2000:])
+
+
 def test_gemm_positioning_in_fused_modes():
     """The fused consumers (XOR checksum, statistics) and the float fills go
     through the same positioning: repeated calls agree with the jump path."""
