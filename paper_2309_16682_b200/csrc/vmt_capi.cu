@@ -1167,7 +1167,9 @@ void build_dephased(int device, cudaStream_t st, std::uint32_t seed0, unsigned n
     DevBuf<std::uint32_t>& dseeds = thread_scratch_u32(device, 0);
     dseeds.reserve(ngen);
     VMT_CUDA(cudaMemcpyAsync(dseeds.p, seeds.data(), ngen * 4, cudaMemcpyHostToDevice, st));
-    vmt_seed_kernel<<<(ngen + 127) / 128, 128, 0, st>>>(dseeds.p, (int)ngen, dst, (long long)kN * L, (int)L);
+    // one warp per CTA: every store of a warp touches 32 different lines (one per
+    // state), so the kernel is bound by the LSUs of the SMs it runs on
+    vmt_seed_kernel<<<(ngen + 31) / 32, 32, 0, st>>>(dseeds.p, (int)ngen, dst, (long long)kN * L, (int)L);
     VMT_CUDA(cudaGetLastError());
     cnt.other += 1;
     // many generators: log2(L) tensor-core GEMMs with cached matrices
@@ -1613,7 +1615,7 @@ int vmt_seed_states(const uint32_t* seeds, uint64_t n, uint32_t* dst, int device
             out.reserve(n * kN);
             o = out.p;
         }
-        vmt_seed_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(ds.p, (int)n, o, kN, 1);
+        vmt_seed_kernel<<<(unsigned)((n + 31) / 32), 32, 0, st>>>(ds.p, (int)n, o, kN, 1);
         VMT_CUDA(cudaGetLastError());
         if (!dev)
             VMT_CUDA(cudaMemcpyAsync(dst, out.p, n * kN * 4, cudaMemcpyDeviceToHost, st));
