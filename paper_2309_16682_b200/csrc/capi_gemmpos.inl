@@ -74,7 +74,8 @@ bool make_tmap_fp4(CUtensorMap& m, const void* base, std::uint64_t rows, unsigne
     const cuuint32_t box[2] = {(cuuint32_t)(kPmKE / 2), box_rows};
     const cuuint32_t estr[2] = {1u, 1u};
     return enc(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, kPmKE == 256 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -93,7 +94,7 @@ bool posmma_pair() {
 // runs alone, fewer beside a generation CTA).
 constexpr int kP2MaxStages = 10;
 int p2_stages_for(int smem_bytes) {
-    for (int s : {10, 8, 7, 6, 5, 4})
+    for (int s : {10, 8, 7, 6, 5, 4, 3, 2})
         if (p2_smem(s) <= smem_bytes)
             return s;
     return 0;
@@ -134,6 +135,14 @@ unsigned long long* timeline_buf() {
     return buf;
 }
 #endif
+
+// (ring depths whose shared memory no CTA can have are never launched: p2_stages_for)
+constexpr int kSmemPerCtaMax = 227 * 1024;
+template <int S>
+void p2_set_smem() {
+    if (p2_smem(S) <= kSmemPerCtaMax)
+        VMT_CUDA(cudaFuncSetAttribute(vmt_posmma2_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, p2_smem(S)));
+}
 
 template <int S>
 void p2_launch(int grid, cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const PosMmaParams& pp) {
@@ -184,18 +193,14 @@ bool posmma_run(GemmPos& gp, const CUtensorMap& tmap_b, const std::uint32_t* src
         std::lock_guard<std::mutex> lk(mu);
         if (!done.count(dev)) {
             VMT_CUDA(cudaFuncSetAttribute(vmt_posmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPmSmem));
-            VMT_CUDA(cudaFuncSetAttribute(vmt_posmma2_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          p2_smem(4)));
-            VMT_CUDA(cudaFuncSetAttribute(vmt_posmma2_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          p2_smem(5)));
-            VMT_CUDA(cudaFuncSetAttribute(vmt_posmma2_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          p2_smem(6)));
-            VMT_CUDA(cudaFuncSetAttribute(vmt_posmma2_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          p2_smem(7)));
-            VMT_CUDA(cudaFuncSetAttribute(vmt_posmma2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          p2_smem(8)));
-            VMT_CUDA(cudaFuncSetAttribute(vmt_posmma2_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          p2_smem(10)));
+            p2_set_smem<2>();
+            p2_set_smem<3>();
+            p2_set_smem<4>();
+            p2_set_smem<5>();
+            p2_set_smem<6>();
+            p2_set_smem<7>();
+            p2_set_smem<8>();
+            p2_set_smem<10>();
             done.insert(dev);
         }
     }
@@ -223,13 +228,18 @@ bool posmma_run(GemmPos& gp, const CUtensorMap& tmap_b, const std::uint32_t* src
     const int tiles = pp.m_tiles * kPmNTiles;
     if (pair) {
         const int grid = 2 * std::min(tiles, sms / 2);
-        switch (stages >= 10 ? 10 : stages >= 8 ? 8 : stages < 4 ? 4 : stages) {
+        // the deepest instantiated ring that is no deeper than asked for and fits a CTA
+        int sg = std::min(stages, p2_stages_for(kSmemPerCtaMax));
+        sg = sg >= 10 ? 10 : sg == 9 ? 8 : sg < 2 ? 2 : sg;
+        switch (sg) {
         case 10: p2_launch<10>(grid, st, gp.pm_tmap_a, tmap_b, pp); break;
         case 8: p2_launch<8>(grid, st, gp.pm_tmap_a, tmap_b, pp); break;
         case 7: p2_launch<7>(grid, st, gp.pm_tmap_a, tmap_b, pp); break;
         case 6: p2_launch<6>(grid, st, gp.pm_tmap_a, tmap_b, pp); break;
         case 5: p2_launch<5>(grid, st, gp.pm_tmap_a, tmap_b, pp); break;
-        default: p2_launch<4>(grid, st, gp.pm_tmap_a, tmap_b, pp); break;
+        case 4: p2_launch<4>(grid, st, gp.pm_tmap_a, tmap_b, pp); break;
+        case 3: p2_launch<3>(grid, st, gp.pm_tmap_a, tmap_b, pp); break;
+        default: p2_launch<2>(grid, st, gp.pm_tmap_a, tmap_b, pp); break;
         }
     } else
         vmt_posmma_kernel<<<std::min(tiles, sms), kPmThreads, kPmSmem, st>>>(gp.pm_tmap_a, tmap_b, pp);

@@ -173,7 +173,7 @@ int posmma_fits(int dev, GenFn fn, int nt, int smem, int per_sm) {
     const int free_smem = sm_smem - per_sm * (smem + 1024) - 1024;
     int stages = single ? (kPmSmem <= free_smem ? kPmStages : 0) : p2_stages_for(free_smem);
     if (const char* cap = std::getenv("VMT_PREF_STAGES")) // experiments: cap the co-resident ring depth
-        stages = std::min(stages, std::max(4, std::atoi(cap)));
+        stages = std::min(stages, std::max(2, std::atoi(cap)));
     const bool ok = stages > 0 && per_sm * regs(ga.numRegs, nt) + regs(pa.numRegs, kPmThreads) <= sm_regs &&
                     per_sm * nt + kPmThreads <= sm_threads && !std::getenv("VMT_NO_TC_PREFETCH");
     if (ok) {
@@ -182,7 +182,9 @@ int posmma_fits(int dev, GenFn fn, int nt, int smem, int per_sm) {
         // would have no room left for the GEMM CTA
         VMT_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                       cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        for (const void* k : {pk, reinterpret_cast<const void*>(vmt_posmma2_kernel<5>),
+        for (const void* k : {pk, reinterpret_cast<const void*>(vmt_posmma2_kernel<2>),
+                              reinterpret_cast<const void*>(vmt_posmma2_kernel<3>),
+                              reinterpret_cast<const void*>(vmt_posmma2_kernel<5>),
                               reinterpret_cast<const void*>(vmt_posmma2_kernel<6>),
                               reinterpret_cast<const void*>(vmt_posmma2_kernel<7>),
                               reinterpret_cast<const void*>(vmt_posmma2_kernel<8>),

@@ -46,8 +46,15 @@ constexpr int kPmNH = VMT_POSMMA_NH;       // output bit columns per MMA (N); 2 
 static_assert((2 * VMT_POSMMA_NH) % 32 == 0 && (kN * 32) % (2 * VMT_POSMMA_NH) == 0 && VMT_POSMMA_NH % 16 == 0,
               "tile = whole state words, tiling 19968 columns");
 constexpr int kPmN = 2 * kPmNH;            // per tile: two MMAs side by side in TMEM = 13 state words
-constexpr int kPmKE = 128;                 // K elements (input bits) per stage = 64 bytes of FP4
-constexpr int kPmStages = 3;
+// K elements (input bits) per stage: 256 = 128 bytes of FP4 per operand row, one
+// whole L2 line per row and TMA box (128-byte swizzle); 128 = 64 bytes (64-byte
+// swizzle, half lines: the round-1/2 shape, kept for A/B builds)
+#ifndef VMT_POSMMA_KE
+#define VMT_POSMMA_KE 256
+#endif
+constexpr int kPmKE = VMT_POSMMA_KE;
+static_assert(kPmKE == 128 || kPmKE == 256, "one swizzle span per operand row and stage");
+constexpr int kPmStages = kPmKE == 256 ? 3 : 3;
 constexpr int kPmABytes = kPmM * kPmKE / 2;        // 8 KB
 constexpr int kPmBHBytes = kPmNH * kPmKE / 2;      // 13 KB per N half
 constexpr int kPmStageBytes = kPmABytes + 2 * kPmBHBytes;
@@ -118,15 +125,17 @@ __device__ __forceinline__ void tc_mma_mxf4(unsigned tmem_d, unsigned long long 
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(tmem_sfa), "r"(tmem_sfb), "r"(accumulate)
         : "memory");
 }
-// K-major operand in the 64-byte swizzle layout: 8-row groups of 8 x 64 B
-// (stride 512 B), 16-byte chunk c of row r at chunk c ^ ((r >> 1) & 3).
+// K-major operand in the swizzled layout of one stage: rows of kPmKE / 2 bytes
+// in 8-row groups (stride 8 rows). 64-byte rows: 16-byte chunk c of row r at
+// chunk c ^ ((r >> 1) & 3) (SWIZZLE_64B); 128-byte rows: at chunk c ^ (r & 7)
+// (SWIZZLE_128B). The K = 64 slices of a stage are 32 bytes apart.
 __device__ __forceinline__ unsigned long long sw64_desc(unsigned saddr) {
     unsigned long long d = 0;
     d |= (unsigned long long)((saddr & 0x3FFFFu) >> 4);  // start address
     d |= (unsigned long long)1 << 16;                     // leading byte offset (unused when swizzled)
-    d |= (unsigned long long)(512 >> 4) << 32;            // stride byte offset: next 8-row group
+    d |= (unsigned long long)((8 * kPmKE / 2) >> 4) << 32; // stride byte offset: next 8-row group
     d |= (unsigned long long)1 << 46;                     // descriptor version (sm_100)
-    d |= (unsigned long long)4 << 61;                     // SWIZZLE_64B
+    d |= (unsigned long long)(kPmKE == 256 ? 2 : 4) << 61; // SWIZZLE_128B / SWIZZLE_64B
     return d;
 }
 // kind::mxf4 instruction descriptor: A and B e2m1 (MXF4 format 1), both
@@ -221,7 +230,7 @@ __global__ void __launch_bounds__(kPmThreads, 1)
                     const unsigned a = smem_u32(smem + s * kPmStageBytes);
                     const unsigned b = a + kPmABytes;
 #pragma unroll
-                    for (int kk = 0; kk < 2; ++kk) { // two K=64 MMAs (32 bytes each) per stage
+                    for (int kk = 0; kk < kPmKE / 64; ++kk) { // K=64 MMAs (32 bytes each) per stage
 #pragma unroll
                         for (int h = 0; h < 2; ++h)
                             tc_mma_mxf4(tmem + kPmNH * h, sw64_desc(a + 32 * kk),
@@ -499,7 +508,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPmThreads, 1)
                     const unsigned a = smem_u32(smem + s * kP2StageBytes);
                     const unsigned b = a + kPmABytes;
 #pragma unroll
-                    for (int kk = 0; kk < 2; ++kk)
+                    for (int kk = 0; kk < kPmKE / 64; ++kk)
 #pragma unroll
                         for (int h = 0; h < 2; ++h)
                             tc_mma_mxf4_pair(tmem + kPmNH * h, sw64_desc(a + 32 * kk),
