@@ -11,6 +11,8 @@ sys.path.insert(0, ".")
 import paper_2309_16682_b200 as V  # noqa: E402
 
 shapes = [(16, 16), (16, 32), (16, 64), (16, 75), (16, 80), (32, 74), (32, 148), (16, 512), (16, 1024)]
+if len(sys.argv) > 2:
+    shapes = [(int(sys.argv[i]), int(sys.argv[i + 1])) for i in range(1, len(sys.argv) - 1, 2)]
 for L, chunks in shapes:
     # a whole number of blocks per chunk so no block advance is needed
     n = chunks * 32 * 624 * L
