@@ -6,10 +6,10 @@
 // ONE GF(2) matrix F^(624 D) (capi_gemmpos.inl): in word-bit coordinates
 //   new[r][j] = sum_i bits(old[r])[i] * M[j][i]  (mod 2),  i, j < 19968.
 // This kernel computes that product while the store-bound generation kernel
-// runs: the generation CTA (one per SM, 108 KB of shared memory, 168
-// registers x 256 threads) leaves ~120 KB of shared memory, 22.5k registers
+// runs: the generation CTA (one per SM at L=32: 86 KB of shared memory, 162
+// registers x 256 threads) leaves ~140 KB of shared memory, 24k registers
 // and the whole tensor core of every SM idle, and one CTA of this kernel
-// (192 threads, 103 KB) fits beside it.
+// (192 threads, a 3-stage operand ring of 130 KB) fits beside it.
 //
 // What it costs the generation kernel is mostly shared-memory bandwidth: the
 // tensor core reads its operands from shared memory, (1/M + 1/N) bytes per
@@ -20,9 +20,10 @@
 // in TMEM, fp32 accumulation -- exact, sums <= 19937), half the bytes of int8.
 //
 // Tile: 128 lane states (M) x 416 output bit columns (two N=208 MMAs side by
-// side in TMEM = 13 whole state words), K staged 128 elements (64 bytes) at
-// a time through a 3-deep ring, both operands by TMA (64-byte swizzle, L2
-// evict_last so the CTAs on the same N slice share B through L2):
+// side in TMEM = 13 whole state words), K staged 256 elements (128 bytes per
+// operand row = one L2 line) at a time through a ring, both operands by TMA
+// (128-byte swizzle, L2 evict_last so the CTAs on the same N slice share B
+// through L2):
 //   warp 0     TMA producer: A = the states' FP4 operand [rows][9984 B]
 //              (vmt_states_to_fp4_kernel), B = F^(624D) FP4 [19968][9984 B]
 //   warp 1     TMEM allocator; one elected lane issues tcgen05.mma
@@ -54,7 +55,7 @@ constexpr int kPmN = 2 * kPmNH;            // per tile: two MMAs side by side in
 #endif
 constexpr int kPmKE = VMT_POSMMA_KE;
 static_assert(kPmKE == 128 || kPmKE == 256, "one swizzle span per operand row and stage");
-constexpr int kPmStages = kPmKE == 256 ? 3 : 3;
+constexpr int kPmStages = 3;              // single-CTA kernel (the pair kernel's depth is a template argument)
 constexpr int kPmABytes = kPmM * kPmKE / 2;        // 8 KB
 constexpr int kPmBHBytes = kPmNH * kPmKE / 2;      // 13 KB per N half
 constexpr int kPmStageBytes = kPmABytes + 2 * kPmBHBytes;
@@ -303,11 +304,10 @@ __global__ void __launch_bounds__(kPmThreads, 1)
 constexpr int kP2BQ = kPmNH / 2;                    // 104 B rows per CTA per MMA
 constexpr int kP2BQBytes = kP2BQ * kPmKE / 2;       // 6656
 constexpr int kP2StageBytes = kPmABytes + 2 * kP2BQBytes; // 21504
-// Operand-ring depth: 4 stages (87 KB) fit beside a 108 KB generation CTA on
-// one SM (the co-resident prefetch); standalone launches (serial
-// positioning, batch de-phasing) and the smaller generation CTAs take deeper
-// rings, which hide more of the TMA latency of the B operand (200 MB, streamed
-// from HBM: it does not fit in L2).
+// Operand-ring depth (stages of 43 KB with the 256-element K stage): 3 fit
+// beside the 86 KB L=32 generation CTA on one SM (the co-resident prefetch), 4
+// beside the L=16 one, 5 when the kernel runs alone (serial positioning, batch
+// de-phasing); the B operand (200 MB) streams from HBM, it does not fit in L2.
 constexpr int kP2Stages = 4;
 __host__ __device__ constexpr int p2_smem(int stages) { return stages * kP2StageBytes + 1024 + 256; }
 constexpr int kP2Smem = p2_smem(kP2Stages);
