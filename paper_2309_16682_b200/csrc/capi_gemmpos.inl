@@ -319,6 +319,27 @@ std::uint64_t usable_base(const GemmPos& gp, std::uint64_t delta) {
 bool gemm_position_exact(vmt_generator* h, GemmPos& gp, const std::uint32_t* src, std::uint32_t* dst,
                          std::uint64_t rows, std::uint64_t delta, cudaStream_t st);
 
+// every state of the `chunks` chunks of states[chunks][624][L] advanced by k blocks in place
+void launch_advance_blocks(std::uint32_t* states, unsigned L, std::uint64_t chunks, int k, cudaStream_t st) {
+    {
+        static std::mutex mu;
+        static std::set<int> done;
+        int dev = 0;
+        VMT_CUDA(cudaGetDevice(&dev));
+        std::lock_guard<std::mutex> lk(mu);
+        if (!done.count(dev)) {
+            VMT_CUDA(cudaFuncSetAttribute(vmt_advance_blocks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          adv_smem(32)));
+            done.insert(dev);
+        }
+    }
+    int lgL = 0;
+    while ((1u << lgL) < L)
+        ++lgL;
+    vmt_advance_blocks_kernel<<<(unsigned)chunks, kAdvThreads, adv_smem((int)L), st>>>(states, lgL, k);
+    VMT_CUDA(cudaGetLastError());
+}
+
 // dst = src jumped by 624*delta words: one GEMM with the matrix of a cached
 // base delta B in [delta-4, delta] (the largest, so exact when cached)
 // followed by delta-B blocks of in-place regeneration (microseconds), or with
@@ -345,10 +366,7 @@ bool gemm_position(vmt_generator* h, GemmPos& gp, const std::uint32_t* src, std:
     if (!gemm_position_exact(h, gp, src, dst, rows, base, st))
         return false;
     if (delta > base) {
-        const unsigned grid = (unsigned)((rows + kAdvWarps - 1) / kAdvWarps);
-        vmt_advance_blocks_kernel<<<grid, 32 * kAdvWarps, 0, st>>>(dst, (int)h->L, (long long)rows,
-                                                                  (int)(delta - base));
-        VMT_CUDA(cudaGetLastError());
+        launch_advance_blocks(dst, h->L, rows / h->L, (int)(delta - base), st);
         h->cnt.other += 1;
     }
     return true;

@@ -970,10 +970,7 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
             if (pref_ready && posmma_launch(*h->gemm, base, h->chunks.p, h->chunks_alt.p, h->L, C * h->L, sms,
                                             h->side, pref_stages, pref_prepared, grid < (std::uint64_t)sms)) {
                 if (delta > base) {
-                    vmt_advance_blocks_kernel<<<(unsigned)((C * h->L + kAdvWarps - 1) / kAdvWarps), 32 * kAdvWarps,
-                                                0, h->side>>>(h->chunks_alt.p, (int)h->L, (long long)(C * h->L),
-                                                              (int)(delta - base));
-                    VMT_CUDA(cudaGetLastError());
+                    launch_advance_blocks(h->chunks_alt.p, h->L, C, (int)(delta - base), h->side);
                     h->cnt.other += 1;
                 }
                 VMT_CUDA(cudaEventRecord(h->ev_pref, h->side));

@@ -213,57 +213,72 @@ __global__ void vmt_states_to_fp4_kernel(const std::uint32_t* __restrict__ st, i
 
 // Advances k whole blocks: every state of an interleaved [C][624][L] array
 // regenerated k times in place (the reference's regenerate,
-// mt19937.cpp:36-49), one warp per lane state in shared memory. The block
+// mt19937.cpp:36-49). One CTA per chunk: the chunk's 624 x L words are one
+// contiguous block, loaded and stored with coalesced 128-byte rows (word i of
+// lane t at [i][t]; a warp per lane state read them at a stride of L words, one
+// sector per word: 40 us for the bench's 4736 states, now ~6). The block
 // splits into the recurrence's dependency phases [0,227), [227,454),
 // [454,623), {623}: inside a phase every new word depends only on words the
 // phase does not write, so each phase is computed into registers and written
-// after a __syncwarp. Used to reuse the positioning matrix of a block delta D
+// after a barrier. Used to reuse the positioning matrix of a block delta D
 // for deltas D+1..D+4.
 namespace vmt_b200 {
 
-constexpr int kAdvWarps = 4;
+constexpr int kAdvThreads = 256;
+constexpr int kAdvMaxItems = (227 * 32 + kAdvThreads - 1) / kAdvThreads; // phase words per thread at L = 32
+__host__ __device__ constexpr int adv_smem(int L) { return kN * L * 4; }
 
-__global__ void __launch_bounds__(32 * kAdvWarps) vmt_advance_blocks_kernel(std::uint32_t* st, int L,
-                                                                           long long nstates, int k) {
-    __shared__ std::uint32_t xs[kAdvWarps][kN];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const long long s = (long long)blockIdx.x * kAdvWarps + w;
-    if (s >= nstates)
-        return;
-    std::uint32_t* x = xs[w];
-    std::uint32_t* g = st + (s / L) * (long long)kN * L + (s % L); // word i at g[i * L]
-    for (int i = lane; i < kN; i += 32)
-        x[i] = g[(long long)i * L];
-    __syncwarp();
+__global__ void __launch_bounds__(kAdvThreads) vmt_advance_blocks_kernel(std::uint32_t* st, int lgL, int k) {
+    extern __shared__ __align__(16) std::uint32_t adv_x[]; // [624][L], L = 2^lgL
+    const int L = 1 << lgL;
+    std::uint32_t* g = st + (long long)blockIdx.x * kN * L;
+    const int total = kN * L;
+    if (lgL >= 2) { // (624 L words: a multiple of 4)
+#pragma unroll 4
+        for (int i = threadIdx.x; i < total / 4; i += kAdvThreads)
+            reinterpret_cast<uint4*>(adv_x)[i] = reinterpret_cast<const uint4*>(g)[i];
+    } else {
+        for (int i = threadIdx.x; i < total; i += kAdvThreads)
+            adv_x[i] = g[i];
+    }
+    __syncthreads();
     for (int r = 0; r < k; ++r) {
-        // phases [0,227), [227,454), [454,623): x[i] = twist(x[i], x[i+1], x[i+397 mod 624])
 #pragma unroll 1
         for (int ph = 0; ph < 3; ++ph) {
-            const int lo = ph * 227, hi = ph == 2 ? kN - 1 : lo + 227;
-            std::uint32_t y[8];
+            const int lo = ph * 227, cnt = (ph == 2 ? kN - 1 - lo : 227) * L; // (word, lane) items of the phase
+            std::uint32_t y[kAdvMaxItems];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int i = lo + lane + 32 * j;
-                if (i < hi) {
+            for (int j = 0; j < kAdvMaxItems; ++j) {
+                const int idx = threadIdx.x + kAdvThreads * j;
+                if (idx < cnt) {
+                    const int i = lo + (idx >> lgL), t = idx & (L - 1);
                     const int im = i + kM < kN ? i + kM : i + kM - kN;
-                    y[j] = twist(x[i], x[i + 1], x[im]);
+                    y[j] = twist(adv_x[i * L + t], adv_x[(i + 1) * L + t], adv_x[im * L + t]);
                 }
             }
-            __syncwarp();
+            __syncthreads();
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int i = lo + lane + 32 * j;
-                if (i < hi)
-                    x[i] = y[j];
+            for (int j = 0; j < kAdvMaxItems; ++j) {
+                const int idx = threadIdx.x + kAdvThreads * j;
+                if (idx < cnt)
+                    adv_x[lo * L + idx] = y[j];
             }
-            __syncwarp();
+            __syncthreads();
         }
-        if (lane == 0)
-            x[kN - 1] = twist(x[kN - 1], x[0], x[kM - 1]);
-        __syncwarp();
+        if ((int)threadIdx.x < L) {
+            const int t = threadIdx.x;
+            adv_x[(kN - 1) * L + t] = twist(adv_x[(kN - 1) * L + t], adv_x[t], adv_x[(kM - 1) * L + t]);
+        }
+        __syncthreads();
     }
-    for (int i = lane; i < kN; i += 32)
-        g[(long long)i * L] = x[i];
+    if (lgL >= 2) {
+#pragma unroll 4
+        for (int i = threadIdx.x; i < total / 4; i += kAdvThreads)
+            reinterpret_cast<uint4*>(g)[i] = reinterpret_cast<const uint4*>(adv_x)[i];
+    } else {
+        for (int i = threadIdx.x; i < total; i += kAdvThreads)
+            g[i] = adv_x[i];
+    }
 }
 
 // Advances every state of a [n][624] array by its own small step count
