@@ -171,11 +171,9 @@ bool posmma_prepare(GemmPos& gp, const std::uint32_t* src, unsigned L, std::uint
         gp.pm_tmap_ptr = gp.pm_a.p;
         gp.pm_tmap_rows = rows_pad;
     }
-    if (rows_pad > rows)
-        VMT_CUDA(cudaMemsetAsync(gp.pm_a.p + rows * kWB / 2, 0, (rows_pad - rows) * kWB / 2, st));
-    const long long nwords = (long long)rows * kN;
-    vmt_states_to_fp4_kernel<<<(unsigned)((nwords + 255) / 256), 256, 0, st>>>(
-        src, (int)L, 0, (int)nl, nwords, reinterpret_cast<std::uint8_t*>(gp.pm_a.p));
+    const long long nthreads = (long long)rows_pad * (kN / 8);
+    vmt_states_to_fp4_kernel<<<(unsigned)((nthreads + 127) / 128), 128, 0, st>>>(
+        src, (int)L, 0, (int)nl, (long long)rows, (long long)rows_pad, reinterpret_cast<std::uint8_t*>(gp.pm_a.p));
     VMT_CUDA(cudaGetLastError());
     return true;
 }

@@ -180,33 +180,60 @@ __global__ void vmt_gemm_matrix_fp4_kernel(const std::uint64_t* __restrict__ row
 }
 
 // a[r][.] for r = c*nl + j: lane lane0+j of state c of an interleaved
-// [C][624][L] array (nl = L, lane0 = 0: every lane state).
+// [C][624][L] array (nl = L, lane0 = 0: every lane state), rows [rows,
+// rows_pad) zeroed. One thread per row and group of 8 state words: 8 reads
+// coalesced across the lanes of a warp, one whole 128-byte line written (one
+// word per thread wrote 16-byte pieces of 32 different lines per warp).
 __global__ void vmt_states_to_fp4_kernel(const std::uint32_t* __restrict__ st, int L, int lane0, int nl,
-                                         long long nwords, std::uint8_t* __restrict__ a) {
+                                         long long rows, long long rows_pad, std::uint8_t* __restrict__ a) {
+    constexpr int kG = kN / 8; // 78 groups of 8 words per row
     const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= nwords)
+    if (idx >= rows_pad * kG)
         return;
-    const int j = (int)(idx % nl);
-    const long long ck = idx / nl;
-    const int k = (int)(ck % kN);
-    const long long c = ck / kN;
-    const long long r = c * nl + j;
-    std::uint32_t w = st[(c * kN + k) * L + lane0 + j];
-    if (k == 0)
-        w &= kUpperMask;
-    // byte n holds bits 2n (low nibble) and 2n+1 (high nibble) as code 0x2
-    std::uint32_t q[4];
+    // consecutive threads: consecutive lanes j of one (state, word group), then word groups, then states
+    long long r;
+    int k8;
+    const long long live = rows * kG;
+    uint4* dst;
+    if (idx < live) {
+        const int j = (int)(idx % nl);
+        const long long cg = idx / nl;
+        k8 = (int)(cg % kG);
+        const long long c = cg / kG;
+        r = c * nl + j;
+        dst = reinterpret_cast<uint4*>(a + r * (kWB / 2) + 128 * k8);
+        const std::uint32_t* src = st + (c * kN + 8 * k8) * L + lane0 + j;
+        std::uint32_t ws[8]; // all eight loads in flight before the first conversion
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-        std::uint32_t v = 0;
+        for (int kk = 0; kk < 8; ++kk)
+            ws[kk] = __ldg(src + (long long)kk * L);
 #pragma unroll
-        for (int n = 0; n < 4; ++n) {
-            const std::uint32_t b = (w >> (8 * m + 2 * n)) & 3u;
-            v |= (((b & 1u) << 1) | ((b & 2u) << 4)) << (8 * n);
+        for (int kk = 0; kk < 8; ++kk) {
+            std::uint32_t w = ws[kk];
+            if (k8 == 0 && kk == 0)
+                w &= kUpperMask;
+            // byte n holds bits 2n (low nibble) and 2n+1 (high nibble) as code 0x2:
+            // bit i of each byte of w moves to bit 4i+1 of a 32-bit word
+            std::uint32_t q[4];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                std::uint32_t x = (w >> (8 * m)) & 0xFFu;
+                x = (x | (x << 12)) & 0x000F000Fu;
+                x = (x | (x << 6)) & 0x03030303u;
+                x = (x | (x << 3)) & 0x11111111u;
+                q[m] = x << 1;
+            }
+            dst[kk] = make_uint4(q[0], q[1], q[2], q[3]);
         }
-        q[m] = v;
+    } else {
+        const long long p = idx - live;
+        r = rows + p / kG;
+        k8 = (int)(p % kG);
+        dst = reinterpret_cast<uint4*>(a + r * (kWB / 2) + 128 * k8);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+            dst[kk] = make_uint4(0u, 0u, 0u, 0u);
     }
-    *reinterpret_cast<uint4*>(a + r * (kWB / 2) + 16 * k) = make_uint4(q[0], q[1], q[2], q[3]);
 }
 
 } // namespace vmt_b200
