@@ -371,3 +371,27 @@ def test_gemm_positioning_small_row_counts(L, chunks, n, prefetch):
         assert gem.prefetch_stats()["used"] >= 2
     else:
         assert gem.positioning_stats()["gemm_positionings"] >= 2
+
+
+@pytest.mark.parametrize("L,chunks,n", [(1, 300, (1 << 22) + 5), (2, 296, (1 << 23) + 77), (4, 148, (1 << 24) + 1),
+                                         (8, 296, (1 << 25) + 4097)])
+def test_gemm_positioning_and_block_advance_at_small_lane_counts(L, chunks, n):
+    """GEMM positioning with the in-place block advance (fill sizes that are
+    not a multiple of the block: every repeat regenerates one or two blocks
+    after the GEMM) at 1, 2, 4 and 8 lanes -- the advance kernel's scalar
+    (L < 4) and 16-byte paths -- against the polynomial jumps."""
+    ref = V.VmtGenerator(1234, V.VmtConfig(L))
+    gem = V.VmtGenerator(1234, V.VmtConfig(L))
+    for g in (ref, gem):
+        g.set_tuning(max_chunks=chunks)
+        g.set_prefetch(0)
+    ref.set_positioning(1)
+    gem.set_positioning(2)
+    a = torch.empty(n, dtype=torch.uint32, device="cuda")
+    b = torch.empty(n, dtype=torch.uint32, device="cuda")
+    for i in range(8):
+        ref.fill_u32(a)
+        gem.fill_u32(b)
+        torch.cuda.synchronize()
+        assert torch.equal(i32(a), i32(b)), (L, chunks, n, i)
+    assert gem.positioning_stats()["gemm_positionings"] >= 3, gem.positioning_stats()
