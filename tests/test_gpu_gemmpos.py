@@ -395,3 +395,17 @@ def test_gemm_positioning_and_block_advance_at_small_lane_counts(L, chunks, n):
         torch.cuda.synchronize()
         assert torch.equal(i32(a), i32(b)), (L, chunks, n, i)
     assert gem.positioning_stats()["gemm_positionings"] >= 3, gem.positioning_stats()
+
+
+def test_randomised_positioning_stress():
+    """profiles/scripts/stress_positioning.py: 150 random fills over four
+    generators (L = 32/16/8/16) with shape changes, skips and chunk-count
+    changes between them -- prefetched, serial-GEMM and jump-positioned fills in
+    whatever order they fall -- every fill identical to jump positioning."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "profiles", "scripts", "stress_positioning.py"), "150", "4"],
+                       cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.startswith("ok"), (r.stdout[-500:], r.stderr[-2000:])
