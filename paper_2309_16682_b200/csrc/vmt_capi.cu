@@ -639,9 +639,9 @@ cudaEvent_t* prof_next(vmt_generator* h) {
 //  * positioning by polynomial jumps (a fill shape seen for the first time):
 //    0.43 us of whole-GPU throughput per lane jump, latency floor 0.16-0.5 ms.
 //  * positioning by the FP4 GEMM (the previous fill had the same size):
-//    ~0.03 ms + 47 us per 256-state x 416-column tile and SM pair, in whole
-//    rounds of sms/2 tiles when it runs alone (1024 rows 0.17 ms, 4736 rows
-//    0.65 ms).
+//    ~0.03 ms + 40 us per 256-state x 416-column tile and SM pair, in whole
+//    rounds of sms/2 tiles when it runs alone (1024 rows 0.15 ms, 4736 rows
+//    0.55 ms).
 //  * `overlap`: that GEMM will run beside the generation kernel as the
 //    tensor-core prefetch of the next fill. One chunk per SM: the two share
 //    the SMs' shared-memory bandwidth, measured t = max(t_gen + 0.5 t_pos,
@@ -675,7 +675,7 @@ std::uint64_t plan_chunks(unsigned L, std::uint64_t n, std::uint64_t c_max, int 
     auto t_pos = [&](std::uint64_t C) -> double { // serial positioning
         const double rows = double(C) * L;
         if (gemm && rows >= (double)gemm_min_rows())
-            return std::min(t_jump(double(C - 1) * L), 0.03e-3 + std::ceil(gemm_tiles(C) / pairs) * 47e-6);
+            return std::min(t_jump(double(C - 1) * L), 0.03e-3 + std::ceil(gemm_tiles(C) / pairs) * 40e-6);
         return t_jump(double(C - 1) * L);
     };
     auto t = [&](std::uint64_t C) {
@@ -684,7 +684,7 @@ std::uint64_t plan_chunks(unsigned L, std::uint64_t n, std::uint64_t c_max, int 
         if (overlap && gemm && double(C) * L >= (double)gemm_min_rows()) {
             if (k > 1)
                 return t_gen + 0.75 * t_pos(C);
-            const double tp = (0.03e-3 + gemm_tiles(C) / pairs * 47e-6) * (L == 32 ? 1.15 : 1.0);
+            const double tp = (0.03e-3 + gemm_tiles(C) / pairs * 40e-6) * (L == 32 ? 1.15 : 1.0);
             return std::max(t_gen + 0.5 * tp, tp + 0.4 * t_gen);
         }
         return t_pos(C) + t_gen;
