@@ -393,9 +393,12 @@ def extras(dev) -> dict:
     s = timed(lambda: g.fill_u32(buf))
     bd = fill_breakdown(g, lambda: g.fill_u32(buf))
     out["c1_L16_2p26_u32"] = {"value": n / s, "unit": "uint32/s", "ms": s * 1e3, "roofline": stated(
-        hbm(n * 4, s), bd, "generation kernel (HBM stores)",
-        "positioning GEMM: every fill re-positions all C x 16 chunk lane states (1200 rows x 19968^2 FP4 MACs, "
-        "~0.23 ms alone, co-resident with the 0.11-0.18 ms generation kernel); see DESIGN.md section 6")}
+        hbm(n * 4, s), bd,
+        "generation kernel sharing each SM's shared-memory bandwidth with the co-resident positioning GEMM of the "
+        "next fill: 60 chunks x 16 lanes = 960 lane states x 19968^2 FP4 MACs (~0.14 ms alone) beside a "
+        "generation kernel that takes ~0.13 ms alone, ~0.175 ms together; see DESIGN.md sections 5-6",
+        "positioning GEMM: every fill re-positions all C x 16 chunk lane states (960 rows x 19968^2 FP4 MACs, "
+        "~0.14 ms alone, co-resident with the generation kernel); see DESIGN.md section 6")}
     # c2: L=8, seed 42, 2^28 -> float32 and float64 in [0,1)
     n = 1 << 28
     f32 = torch.empty(n, dtype=torch.float32, device=dev)
