@@ -406,8 +406,11 @@ def extras(dev) -> dict:
     s = timed(lambda: g.fill_f32(f32))
     bd = fill_breakdown(g, lambda: g.fill_f32(f32))
     out["c2_L8_2p28_f32"] = {"value": n / s, "unit": "float32/s", "ms": s * 1e3, "gbs": n * 4 / s / 1e9,
-                             "roofline": stated(hbm(n * 4, s), bd, "generation kernel (HBM stores)",
-                                                "positioning GEMM (296 chunks x 8 lanes = 2368 rows per fill)")}
+                             "roofline": stated(hbm(n * 4, s), bd,
+                                                "generation kernel: 148 chunks x 8 lanes, one lane per thread = 4 warps "
+                                                "per SM (latency-bound: ~0.26 ms alone), sharing the SM with the "
+                                                "co-resident positioning GEMM of 1184 lane states",
+                                                "positioning GEMM (148 chunks x 8 lanes = 1184 rows per fill)")}
     del f32
     f64 = torch.empty(n, dtype=torch.float64, device=dev)
     s = timed(lambda: g.fill_f64(f64))
@@ -415,7 +418,8 @@ def extras(dev) -> dict:
     out["c2_L8_2p28_f64"] = {"value": n / s, "unit": "float64/s", "ms": s * 1e3, "gbs": n * 8 / s / 1e9,
                              "roofline": stated(hbm(n * 8, s), bd,
                                                 "generation kernel: 8-byte elements, one double per word "
-                                                "(I2F.F64 + DMUL per word, 148 chunks)",
+                                                "(I2F.F64 + DMUL per word, 148 chunks, 4 warps per SM), beside the "
+                                                "co-resident positioning GEMM of 1184 lane states",
                                                 "positioning GEMM (148 chunks x 8 lanes = 1184 rows per fill)")}
     del f64
     # c3: 1024 generators (L=16, seeds 1..1024, full period) x 2^20 words, generator-major,
