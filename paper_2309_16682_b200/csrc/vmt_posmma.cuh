@@ -71,6 +71,16 @@ constexpr int kPmSfCol = 448;              // TMEM columns [448, 512): unit scal
 __device__ __forceinline__ std::uint32_t parity_bit(std::uint32_t acc) {
     return __float_as_uint(__uint_as_float(acc) + 8388608.0f) & 1u;
 }
+// The 32 parities of v[0..31] as one word, bit b from v[b]: each step shifts
+// the word right by one and takes the lowest mantissa bit of v[b] + 2^23 in at
+// bit 31 (one FADD + one funnel shift per bit instead of FADD, AND, SHL, OR)
+__device__ __forceinline__ std::uint32_t parity_word(const std::uint32_t (&v)[32]) {
+    std::uint32_t w = 0;
+#pragma unroll
+    for (int b = 0; b < 32; ++b)
+        w = __funnelshift_r(w, __float_as_uint(__uint_as_float(v[b]) + 8388608.0f), 1);
+    return w;
+}
 
 struct PosMmaParams {
     std::uint32_t* dst;       // [C][624][L] jumped by the matrix (the next fill's)
@@ -270,10 +280,7 @@ __global__ void __launch_bounds__(kPmThreads, 1)
                       "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
                     : "r"(tmem + ((unsigned)rq << 16) + 32u * j));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                std::uint32_t w = 0;
-#pragma unroll
-                for (int b = 0; b < 32; ++b) // exact fp32 sums of 0/1 products: bit = parity
-                    w |= parity_bit(v[b]) << b;
+                const std::uint32_t w = parity_word(v); // exact fp32 sums of 0/1 products: bit = parity
                 const int k = n * (kPmN / 32) + j;
                 if (valid)
                     dst[(long long)k * p.L] = k == 0 ? (w & kUpperMask) : w;
@@ -548,10 +555,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPmThreads, 1)
                       "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
                     : "r"(tmem + ((unsigned)rq << 16) + 32u * j));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                std::uint32_t w = 0;
-#pragma unroll
-                for (int b = 0; b < 32; ++b)
-                    w |= parity_bit(v[b]) << b;
+                const std::uint32_t w = parity_word(v);
                 const int k = n * (kPmN / 32) + j;
                 if (valid)
                     dst[(long long)k * p.L] = k == 0 ? (w & kUpperMask) : w;
