@@ -46,6 +46,11 @@ struct GemmPos {
     std::map<std::uint64_t, CUtensorMap> tmaps2; // 104-row boxes for the CTA-pair kernel
     DevBuf<std::int8_t> pm_a; // FP4 state operand
     DevBuf<unsigned> pm_ctr;  // tile counter of the pair kernel's scheduler (vmt_posmma.cuh)
+    // pm_a already holds the operand of these states (written at the end of the
+    // prefetch that produced them): consumed or dropped by the next posmma_prepare
+    const void* fp4_src = nullptr;
+    std::uint64_t fp4_rows = 0;
+    unsigned fp4_nl = 0;
     CUtensorMap pm_tmap_a;
     const void* pm_tmap_ptr = nullptr;
     std::uint64_t pm_tmap_rows = 0;
@@ -164,6 +169,11 @@ bool posmma_prepare(GemmPos& gp, const std::uint32_t* src, unsigned L, std::uint
                     unsigned nl) {
     const std::uint64_t tile_rows = posmma_pair() ? 2 * kPmM : kPmM;
     const std::uint64_t rows_pad = (rows + tile_rows - 1) / tile_rows * tile_rows;
+    const bool ready = gp.fp4_src == src && gp.fp4_rows == rows && gp.fp4_nl == nl && gp.pm_a.p &&
+                       gp.pm_tmap_ptr == gp.pm_a.p && gp.pm_tmap_rows == rows_pad;
+    gp.fp4_src = nullptr; // one use: the buffer is rewritten by whatever is prepared next
+    if (ready)
+        return true;
     gp.pm_a.reserve(rows_pad * kWB / 2);
     if (gp.pm_tmap_ptr != gp.pm_a.p || gp.pm_tmap_rows != rows_pad) {
         if (!make_tmap_fp4(gp.pm_tmap_a, gp.pm_a.p, rows_pad, kPmM))

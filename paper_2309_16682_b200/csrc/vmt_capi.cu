@@ -834,6 +834,8 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
         }
     }
     if (!positioned) {
+        if (h->gemm)
+            h->gemm->fp4_src = nullptr; // the chunk buffers are rewritten by the jumps
         reposition(h, b0, st);
         h->chunks.reserve((size_t)C * kN * h->L);
         VMT_CUDA(cudaMemcpyAsync(h->chunks.p, h->cur.p, (size_t)kN * h->L * 4, cudaMemcpyDeviceToDevice, st));
@@ -972,6 +974,17 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
                 if (delta > base) {
                     launch_advance_blocks(h->chunks_alt.p, h->L, C, (int)(delta - base), h->side);
                     h->cnt.other += 1;
+                }
+                // the operand of the NEXT fill's GEMM (these states) right behind them on
+                // the side stream instead of ahead of the next generation kernel on the
+                // fill's stream: hidden whenever the prefetch ends before the generation
+                if (pref_prepared && !std::getenv("VMT_NO_EAGER_FP4")) {
+                    GemmPos& gp = *h->gemm;
+                    if (posmma_prepare(gp, h->chunks_alt.p, h->L, C * h->L, h->side, h->L)) {
+                        gp.fp4_src = h->chunks_alt.p;
+                        gp.fp4_rows = C * h->L;
+                        gp.fp4_nl = h->L;
+                    }
                 }
                 VMT_CUDA(cudaEventRecord(h->ev_pref, h->side));
                 h->pref_valid = true;
