@@ -119,12 +119,13 @@ print("ok")
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("tiles,prep", [("1", "1"), ("2", "2"), ("1", "2"), ("2", "1")])
-def test_tile_scheduler_and_operand_modes(tiles, prep):
+@pytest.mark.parametrize("tiles,prep,eager", [("1", "1", True), ("2", "2", True), ("1", "2", True), ("2", "1", True),
+                                              ("1", "1", False)])
+def test_tile_scheduler_and_operand_modes(tiles, prep, eager):
     """The pair kernel's tile order (VMT_POSMMA_TILES: 1 = from the global
     counter, 2 = static round-robin) and the stream its FP4 operand is written
-    on (VMT_PREP_AHEAD: 1 = ahead of the generation kernel, 2 = side stream)
-    never change a word: co-resident prefetch with fewer chunks than SMs, one
+    on (VMT_PREP_AHEAD: 1 = ahead of the generation kernel, 2 = side stream;
+    VMT_NO_EAGER_FP4: not right behind the previous prefetch) never change a word: co-resident prefetch with fewer chunks than SMs, one
     chunk per SM, ragged fill sizes and a serial GEMM, against the polynomial
     jumps."""
     import os
@@ -151,7 +152,8 @@ print("ok")
 '''
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
-                       env=dict(os.environ, VMT_POSMMA_TILES=tiles, VMT_PREP_AHEAD=prep))
+                       env=dict(os.environ, VMT_POSMMA_TILES=tiles, VMT_PREP_AHEAD=prep,
+                                **({} if eager else {"VMT_NO_EAGER_FP4": "1"})))
     assert r.returncode == 0 and "ok" in r.stdout, (r.stdout[-500:], r.stderr[-2000:])
 
 
