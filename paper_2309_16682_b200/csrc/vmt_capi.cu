@@ -1595,7 +1595,7 @@ int vmt_jump_states(const uint32_t* src, uint64_t n, const uint64_t* distances, 
         DevBuf<unsigned long long>& dd = thread_scratch<unsigned long long>(device, 5);
         dd.reserve(n);
         VMT_CUDA(cudaMemcpyAsync(dd.p, d.data(), n * 8, cudaMemcpyHostToDevice, st));
-        vmt_advance_steps_kernel<<<(unsigned)((n + kStepWarps - 1) / kStepWarps), 32 * kStepWarps, 0, st>>>(
+        vmt_advance_steps_kernel<<<(unsigned)n, kStepThreads, 0, st>>>(
             buf.p, (long long)n, dd.p, 0xFFFFu);
         VMT_CUDA(cudaGetLastError());
         if (is_device_ptr(dst))

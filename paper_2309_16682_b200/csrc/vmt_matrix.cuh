@@ -315,38 +315,52 @@ __global__ void __launch_bounds__(kAdvThreads) vmt_advance_blocks_kernel(std::ui
 // old). Word 0 of the result keeps only its live bit, as the polynomial jump's
 // output does (mt19937.cpp:79), also for r = 0. ~13x cheaper than a polynomial jump for
 // r < 2^16; vmt_jump_states uses it for the low 16 bits of each distance.
-constexpr int kStepWarps = 4;
-__global__ void __launch_bounds__(32 * kStepWarps) vmt_advance_steps_kernel(std::uint32_t* st, long long nstates,
-                                                                           const unsigned long long* steps,
-                                                                           unsigned mask) {
-    __shared__ std::uint32_t ring[kStepWarps][1024];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const long long s = (long long)blockIdx.x * kStepWarps + w;
+constexpr int kStepThreads = 256;
+constexpr int kStepPhases = 8;                    // phases generated linearly before the window moves back
+constexpr int kStepBuf = kN + 227 * kStepPhases;  // words per state
+__global__ void __launch_bounds__(kStepThreads) vmt_advance_steps_kernel(std::uint32_t* st, long long nstates,
+                                                                        const unsigned long long* steps,
+                                                                        unsigned mask) {
+    // One CTA per state: the window x_0..x_623 followed by up to 8 phases of
+    // new words, x_{624+k} = twist(x_k, x_{k+1}, x_{k+397}), thread t computing
+    // word t of each 227-word phase (one barrier per phase); after 8 phases
+    // the last 624 words move back to the front. A warp per state (8 rounds
+    // per phase, ring masks) was latency-bound at ~16% occupancy with a long
+    // tail behind the largest step counts: 4096 states with 16-bit step
+    // counts 0.25 ms.
+    __shared__ std::uint32_t x[kStepBuf];
+    const int t = threadIdx.x;
+    const long long s = blockIdx.x;
     if (s >= nstates)
         return;
     const int r = (int)(steps[s] & mask);
-    std::uint32_t* x = ring[w];
     std::uint32_t* g = st + s * kN;
     if (r == 0) { // the effective state: dead bits of word 0 cleared (mt19937.cpp:79)
-        if (lane == 0)
+        if (t == 0)
             g[0] &= kUpperMask;
         return;
     }
-    for (int i = lane; i < kN; i += 32)
+    for (int i = t; i < kN; i += kStepThreads)
         x[i] = g[i];
-    __syncwarp();
-    for (int n = kN; n < r + kN; n += 227) {
-        const int cnt = min(227, r + kN - n);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int i = n + lane + 32 * j; // x_i from x_{i-624}, x_{i-623}, x_{i-227}
-            if (lane + 32 * j < cnt)
-                x[i & 1023] = twist(x[(i - kN) & 1023], x[(i - kN + 1) & 1023], x[(i - kN + kM) & 1023]);
+    __syncthreads();
+    int produced = 0, batch = 0;
+    for (;;) {
+        batch = min(r - produced, 227 * kStepPhases);
+        for (int base = 0; base < batch; base += 227) {
+            if (t < min(227, batch - base))
+                x[kN + base + t] = twist(x[base + t], x[base + t + 1], x[base + t + kM]);
+            __syncthreads();
         }
-        __syncwarp();
+        produced += batch;
+        if (produced >= r)
+            break;
+        // a whole batch (1816 >= 624 new words): the last 624 words become the window
+        for (int i = t; i < kN; i += kStepThreads)
+            x[i] = x[batch + i];
+        __syncthreads();
     }
-    for (int i = lane; i < kN; i += 32) {
-        const std::uint32_t v = x[(r + i) & 1023];
+    for (int i = t; i < kN; i += kStepThreads) {
+        const std::uint32_t v = x[batch + i];
         g[i] = i == 0 ? (v & kUpperMask) : v;
     }
 }
