@@ -684,7 +684,7 @@ cudaEvent_t* prof_next(vmt_generator* h) {
 //    the SMs' shared-memory bandwidth, measured t = max(t_gen + 0.5 t_pos,
 //    t_pos + 0.4 t_gen) with the tiles handed out dynamically (no whole
 //    rounds; 15% slower beside the 86 KB L=32 CTA, whose neighbour gets a
-//    shallower operand ring). More chunks per SM: t_gen + 0.75 t_pos.
+//    shallower operand ring). More chunks per SM: t_gen + t_pos.
 // Fused XOR fills (no stores) run at ~5.5e8 words/s per lane and saturate at
 // ~3.4e12 words/s per GPU.
 #ifndef VMT_PLAN_RLANE
@@ -705,8 +705,12 @@ std::uint64_t plan_chunks(unsigned L, std::uint64_t n, std::uint64_t c_max, int 
     const bool dbl = mode == MODE_F64 || mode == MODE_F64_REAL3;
     // lane_speed: threads per lane of the kernel shape relative to the R=13,
     // VW=2 shape (VW=1 has twice as many and runs a lane 1.6x as fast)
-    const double r_lane = fused ? 5.5e8 * lane_speed : VMT_PLAN_RLANE * (1.0 + 0.6 * (std::min(lane_speed, 2.0) - 1.0)),
-                 peak_sm = (fused ? 3.4e12 : dbl ? 5.1e11 : 1.6e12) / 148.0;
+    // (the one-lane kernel runs 208 threads on its lane: 1.8e9 words/s)
+    const double r_lane = fused ? 5.5e8 * lane_speed
+                          : lane_speed > 8.0 ? 1.8e9
+                                             : VMT_PLAN_RLANE * (1.0 + 0.6 * (std::min(lane_speed, 2.0) - 1.0)),
+                 // (1- and 2-lane kernels saturate an SM at ~3e9 words/s: measured 2.3-2.9e9 with 2-4 CTAs per SM)
+                 peak_sm = fused ? 3.4e12 / 148.0 : dbl ? 5.1e11 / 148.0 : L <= 2 ? 3.0e9 : 1.6e12 / 148.0;
     const double pairs = std::max(1, sms / 2);
     auto gemm_tiles = [&](std::uint64_t C) { return std::ceil(double(C) * L / 256.0) * 48.0; };
     auto t_pos = [&](std::uint64_t C) -> double { // serial positioning
@@ -719,8 +723,8 @@ std::uint64_t plan_chunks(unsigned L, std::uint64_t n, std::uint64_t c_max, int 
         const double k = (double)((C + sms - 1) / sms);
         const double t_gen = (double(n) / double(C)) / std::min(L * r_lane, peak_sm / k);
         if (overlap && gemm && double(C) * L >= (double)gemm_min_rows()) {
-            if (k > 1)
-                return t_gen + 0.75 * t_pos(C);
+            if (k > 1) // (beside several generation CTAs per SM the GEMM hides nothing: measured at L = 2, 8, 16)
+                return t_gen + t_pos(C);
             const double tp = (0.03e-3 + gemm_tiles(C) / pairs * 40e-6) * (L == 32 ? 1.15 : 1.0);
             return std::max(t_gen + 0.5 * tp, tp + 0.4 * t_gen);
         }
