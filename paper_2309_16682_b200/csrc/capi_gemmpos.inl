@@ -353,10 +353,16 @@ void launch_advance_blocks(std::uint32_t* states, unsigned L, std::uint64_t chun
 // followed by delta-B blocks of in-place regeneration (microseconds), or with
 // a new matrix built for delta -- a fill size alternating between block
 // deltas D and D+1 then needs one matrix when D repeats first.
+// floor_delta: floor(words between the starts of consecutive fills / block), when
+// the caller knows it (0: unknown) -- the block deltas of such a sequence are
+// floor_delta and floor_delta + 1, so a matrix for floor_delta serves both and
+// the fills whose delta is the floor need no advance at all.
 bool gemm_position(vmt_generator* h, GemmPos& gp, const std::uint32_t* src, std::uint32_t* dst, std::uint64_t rows,
-                   std::uint64_t delta, cudaStream_t st) {
+                   std::uint64_t delta, cudaStream_t st, std::uint64_t floor_delta = 0) {
     std::uint64_t base = usable_base(gp, delta);
-    if (base == 0) {
+    if (base == 0 && floor_delta != 0 && (floor_delta == delta || floor_delta + 1 == delta)) {
+        base = floor_delta;
+    } else if (base == 0) {
         // no matrix yet: build it for the smallest recently seen delta in
         // [delta-4, delta], and at most delta-1: fills of n words alternate
         // between block deltas floor(n/bw) and floor(n/bw)+1 in whichever

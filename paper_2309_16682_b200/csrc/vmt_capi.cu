@@ -857,7 +857,11 @@ void gpu_generate(vmt_generator* h, int mode, void* out, std::uint64_t n, cudaSt
             if (usable_base(gp, delta) || seen >= 2 || h->positioning == 2) {
                 h->chunks_alt.reserve((size_t)C * kN * h->L);
                 try {
-                    if (gemm_position(h, gp, h->chunks.p, h->chunks_alt.p, C * h->L, delta, st)) {
+                    // words between this fill's start and the previous one's (same size: repeat)
+                    std::uint64_t floor_delta = 0;
+                    if (repeat && h->last_end != ~0ull && h->last_end >= n && P0 + n > h->last_end)
+                        floor_delta = (P0 - (h->last_end - n)) / h->bw;
+                    if (gemm_position(h, gp, h->chunks.p, h->chunks_alt.p, C * h->L, delta, st, floor_delta)) {
                         h->chunks.swap(h->chunks_alt);
                         positioned = true;
                     }
