@@ -231,7 +231,7 @@ int vmt_set_prefetch(vmt_handle h, int enable);
 /* Chunk positioning of consecutive fills: mode 0 =
  * auto (one FP4 tensor-core GEMM -- our tcgen05 kernel -- maps the previous
  * fill's chunk states to the next fill's when the
- * fill shape and block delta repeat and there are at least 1024 lane states;
+ * fill shape and block delta repeat and there are at least 256 lane states;
  * polynomial jumps otherwise), 1 = polynomial jumps only, 2 = GEMM whenever
  * the shape repeats. Results are identical. */
 int vmt_set_positioning(vmt_handle h, int mode);
@@ -241,7 +241,9 @@ int vmt_positioning_stats(vmt_handle h, uint64_t* gemm_positionings, uint64_t* c
 int vmt_prefetch_stats(vmt_handle h, uint64_t* tensor_prefetches, uint64_t* used);
 /* De-phasing of many generators at once (vmt_batch_*, >= 4096 lane states)
  * runs as log2(lanes) FP4 GEMMs with a process-wide cache of the jump
- * matrices F^(s 2^q) per device (200 MB each, at most 8); this frees it. */
+ * matrices F^(s 2^q) per device (200 MB each, at most 8); this frees it,
+ * and the process-wide host caches of the seed-independent polynomials
+ * (de-phasing polynomials per (q, lanes), chunk polynomials per chunk size). */
 int vmt_release_caches(int device);
 
 /* Profiling: when enabled, each fill records CUDA events on its stream around
